@@ -1,0 +1,219 @@
+"""ctypes wrapper of the CPU oracle (oracle/hpfem_oracle.cpp).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py.  The product package
+(paper_2402_11299_b200) never imports it, and this package never imports the
+product.  Every function cites the passage of PAPER.md it follows in the C++
+source; readings are listed in DESIGN.md.
+
+Parity status: every function exported here is pinned by tests/test_oracle_pins.py
+against values fixed by the paper or by mathematics (quadrature, dense LAPACK,
+mpmath, closed forms); none is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hpfem_oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC"]
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (g++ -O2 -ffp-contract=off, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", *CFLAGS, "-o", tmp, _SRC, "-lquadmath"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        _declare(_lib)
+    return _lib
+
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+_d = ctypes.c_double
+_i = ctypes.c_int
+
+
+def _declare(L):
+    L.oracle_last_error.restype = ctypes.c_char_p
+    L.oracle_dim.argtypes = [_i, _i, _i]
+    L.oracle_operator_dense.argtypes = [_dp, _i, _i, _i, _d, _d, _dp]
+    L.oracle_operator_coo.argtypes = [_dp, _i, _i, _i, _i, _ip, _ip, _dp, _ip]
+    L.oracle_factor_dense.argtypes = [_dp, _i, _i, _i, _d, _d, _dp, _ip]
+    L.oracle_solve1d.argtypes = [_dp, _i, _i, _i, _d, _d, _dp, _dp, _i]
+    L.oracle_spectrum.argtypes = [_dp, _i, _i, _i, _d, _dp]
+    L.oracle_shifts.argtypes = [_d, _d, _d, _d, _d, _i, _ip, _dp, _dp, _dp]
+    L.oracle_plan.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _d, _i, _ip, _dp, _dp, _dp, _dp, _dp]
+    L.oracle_adi_solve.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _d, _dp, _dp, _i, _ip]
+    L.oracle_apply.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _dp, _dp]
+    L.oracle_load.argtypes = [_dp, _i, _i, _dp, _i, _i, _i, _dp, _dp]
+    for f in ("oracle_operator_dense", "oracle_operator_coo", "oracle_factor_dense", "oracle_solve1d",
+              "oracle_spectrum", "oracle_shifts", "oracle_plan", "oracle_adi_solve", "oracle_apply", "oracle_load"):
+        getattr(L, f).restype = _i
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"oracle error {code}: {msg}")
+        self.code = code
+
+
+def _check(rc):
+    if rc != 0:
+        raise OracleError(rc, lib().oracle_last_error().decode())
+
+
+def _ptr(a):
+    return a.ctypes.data_as(_dp)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def dim(n, p, bc):
+    return lib().oracle_dim(n, p, bc)
+
+
+def operator_dense(xs, p, bc, alpha, beta):
+    """Dense alpha*K + beta*M of the 1D space (K = -Delta; M)."""
+    xs = _f64(xs)
+    n = xs.size - 1
+    N = dim(n, p, bc)
+    out = np.empty((N, N))
+    _check(lib().oracle_operator_dense(_ptr(xs), n, p, bc, alpha, beta, _ptr(out)))
+    return out
+
+
+def operator_sparse(xs, p, bc, which):
+    """scipy.sparse CSR of K (which=0) or M (which=1)."""
+    import scipy.sparse as sp
+    xs = _f64(xs)
+    n = xs.size - 1
+    nnz = ctypes.c_int(0)
+    _check(lib().oracle_operator_coo(_ptr(xs), n, p, bc, which, None, None, None, ctypes.byref(nnz)))
+    r = np.empty(nnz.value, dtype=np.int32)
+    c = np.empty(nnz.value, dtype=np.int32)
+    v = np.empty(nnz.value)
+    _check(lib().oracle_operator_coo(_ptr(xs), n, p, bc, which, r.ctypes.data_as(_ip), c.ctypes.data_as(_ip),
+                                     _ptr(v), ctypes.byref(nnz)))
+    N = dim(n, p, bc)
+    return sp.csr_matrix((v, (r, c)), shape=(N, N))
+
+
+def factor_dense(xs, p, bc, alpha, beta):
+    """Dense reverse-Cholesky factor L (A = L^T L, Alg. 1)."""
+    xs = _f64(xs)
+    n = xs.size - 1
+    N = dim(n, p, bc)
+    out = np.empty((N, N))
+    info = (ctypes.c_int * 3)(-1, -1, -1)
+    rc = lib().oracle_factor_dense(_ptr(xs), n, p, bc, alpha, beta, _ptr(out), info)
+    if rc == -2:
+        raise OracleError(rc, f"not positive definite at {tuple(info)}")
+    _check(rc)
+    return out
+
+
+def solve1d(xs, p, bc, alpha, beta, f):
+    """(alpha K + beta M)^{-1} f for f of shape (N,) or (nrhs, N) (Cor. 4.3)."""
+    xs = _f64(xs)
+    n = xs.size - 1
+    f = _f64(f)
+    x = np.empty_like(f)
+    nrhs = 1 if f.ndim == 1 else f.shape[0]
+    _check(lib().oracle_solve1d(_ptr(xs), n, p, bc, alpha, beta, _ptr(f), _ptr(x), nrhs))
+    return x
+
+
+def spectrum(xs, p, bc, omega):
+    """[lambda_min, lambda_max] of the pencil (K + w^2/2 M, M) (reading R4)."""
+    xs = _f64(xs)
+    lam = np.empty(2)
+    _check(lib().oracle_spectrum(_ptr(xs), xs.size - 1, p, bc, omega, _ptr(lam)))
+    return lam
+
+
+def shifts(a, b, c, d, eps, maxJ=4096):
+    """(J, gamma, p[J], q[J]) for sigma(A) in [a,b], sigma(B) in [c,d]
+    (Alg. 2 lines 2-3; reading R5)."""
+    P = np.empty(maxJ)
+    Q = np.empty(maxJ)
+    J = ctypes.c_int(0)
+    g = ctypes.c_double(0)
+    _check(lib().oracle_shifts(a, b, c, d, eps, maxJ, ctypes.byref(J), ctypes.byref(g), _ptr(P), _ptr(Q)))
+    return J.value, g.value, P[:J.value].copy(), Q[:J.value].copy()
+
+
+def plan(xs, px, ys, py, omega, bc, tol, maxJ=4096):
+    xs, ys = _f64(xs), _f64(ys)
+    dims = (ctypes.c_int * 3)()
+    lx, ly, P, Q = np.empty(2), np.empty(2), np.empty(maxJ), np.empty(maxJ)
+    g = ctypes.c_double(0)
+    _check(lib().oracle_plan(_ptr(xs), xs.size - 1, px, _ptr(ys), ys.size - 1, py, omega, bc, tol, maxJ, dims,
+                             _ptr(lx), _ptr(ly), ctypes.byref(g), _ptr(P), _ptr(Q)))
+    J = dims[2]
+    return dict(Nx=dims[0], Ny=dims[1], J=J, lam_x=lx, lam_y=ly, gamma=g.value, p=P[:J].copy(), q=Q[:J].copy())
+
+
+def adi_solve(xs, px, ys, py, omega, bc, tol, G, iters=-1):
+    """Algorithm 2; returns (U, J)."""
+    xs, ys, G = _f64(xs), _f64(ys), _f64(G)
+    U = np.empty_like(G)
+    J = ctypes.c_int(0)
+    _check(lib().oracle_adi_solve(_ptr(xs), xs.size - 1, px, _ptr(ys), ys.size - 1, py, omega, bc, tol, _ptr(G),
+                                  _ptr(U), iters, ctypes.byref(J)))
+    return U, J.value
+
+
+def apply(xs, px, ys, py, omega, bc, U):
+    """A_x U M_y + M_x U A_y (eq. adi:poisson)."""
+    xs, ys, U = _f64(xs), _f64(ys), _f64(U)
+    F = np.empty_like(U)
+    _check(lib().oracle_apply(_ptr(xs), xs.size - 1, px, _ptr(ys), ys.size - 1, py, omega, bc, _ptr(U), _ptr(F)))
+    return F
+
+
+def load(xs, px, ys, py, bc, Fleg):
+    """G = R_x^T M_P,x F_leg M_P,y R_y."""
+    xs, ys, Fleg = _f64(xs), _f64(ys), _f64(Fleg)
+    Nx, Ny = dim(xs.size - 1, px, bc), dim(ys.size - 1, py, bc)
+    G = np.empty((Nx, Ny))
+    _check(lib().oracle_load(_ptr(xs), xs.size - 1, px, _ptr(ys), ys.size - 1, py, bc, _ptr(Fleg), _ptr(G)))
+    return G
+
+
+def l2_norm_sq(xs, px, ys, py, bc, U):
+    """||u||^2_{L2} of the FEM function with coefficients U: tr(U^T M_x U M_y)
+    = ||V U L^T||_F^2 for M_x = V^T V, M_y = L^T L (the Lemma 5.1 norm,
+    P:L733).  Used as the parity norm (reading R12)."""
+    Mx = operator_sparse(xs, px, bc, 1)
+    My = operator_sparse(ys, py, bc, 1)
+    U = _f64(U)
+    A = Mx @ U
+    B = (My @ U.T).T
+    return float(np.einsum("ij,ij->", A, B))
+
+
+def l2_rel_diff(xs, px, ys, py, bc, U, Uref):
+    """||u - u_ref||_{L2} / ||u_ref||_{L2}."""
+    d = l2_norm_sq(xs, px, ys, py, bc, np.asarray(U) - np.asarray(Uref))
+    r = l2_norm_sq(xs, px, ys, py, bc, Uref)
+    return float(np.sqrt(max(d, 0.0) / r))
