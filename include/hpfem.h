@@ -1,0 +1,142 @@
+/*
+ * hpfem.h -- C ABI of the B200-native ADI hp-FEM screened-Poisson solver
+ * (the hot path of arXiv 2402.11299).
+ *
+ * Problem (eq. poisson):  -Laplace(u) + w^2 u = f  on
+ * [a,b] x [c,d] with zero Dirichlet (basis Q) or zero Neumann
+ * (basis C) conditions on all four sides, discretised in the
+ * hat + integrated-Legendre (Babuska-Suri) basis of P:L138-L184 and solved
+ * as the generalised Sylvester equation (eq. 2d:poisson P:L419-L424 /
+ * eq. adi:poisson P:L658-L664)
+ *
+ *        A_x U M_y + M_x U A_y = G,     A_d = K_d + (w^2/2) M_d,
+ *
+ * by the generalised ADI method, Algorithm 2, whose 1D shifted
+ * solves use the reverse Cholesky factorisation of Algorithm 1
+ * (Cor. 4.3 P:L590-L615).
+ *
+ * Layout of every 2D array (U, F, G): fp64, N_x x N_y, row-major, contiguous
+ * (leading dimension N_y); row i = x-dof, column j = y-dof.  Within each
+ * dimension the dofs are ordered degree-major / element-minor as in
+ * the kept hats first (n-1 for Dirichlet, n+1 for Neumann), then
+ * for k = 0..p-2 the n bubbles W_{k,e}, e = 0..n-1.  N = p n - 1 (Dirichlet,
+ * P:L384) or p n + 1 (Neumann).
+ *
+ * Ownership: the caller owns F, U, F_leg (DEVICE pointers, e.g. torch
+ * tensors).  The plan owns its factor tables, shift tables and one N_x x N_y
+ * workspace.  All work is enqueued asynchronously on the stream passed in
+ * (a cudaStream_t; NULL = legacy default stream).  A plan may be used by one
+ * stream at a time (its workspace is shared by its solves).
+ *
+ * Errors: every call returns HPFEM_OK (0) or a negative code; a thread-local
+ * message is available from hpfem_last_error().  Launch failures return
+ * HPFEM_ECUDA immediately; asynchronous device faults surface at the
+ * caller's next synchronisation.  There is no CPU fallback: on a machine
+ * without a usable sm_100 device every call that touches the device returns
+ * HPFEM_ECUDA.
+ */
+#ifndef HPFEM_H_
+#define HPFEM_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hpfem_plan_s* hpfem_plan_t; /* opaque; owned by the library */
+
+enum { HPFEM_BC_DIRICHLET = 0, HPFEM_BC_NEUMANN = 1 }; /* same BC on all four sides */
+
+enum {
+  HPFEM_OK = 0,
+  HPFEM_EINVAL = -1,   /* bad argument: n < 1, p < 2, non-increasing breakpoints,
+                          tol not in (0,1), Neumann with w = 0, aliasing */
+  HPFEM_ENOTPD = -2,   /* a non-positive pivot in a reverse Cholesky factorisation */
+  HPFEM_ECUDA = -3,    /* CUDA runtime / launch error, or no sm_100 device */
+  HPFEM_ENOMEM = -4,   /* device allocation failed */
+  HPFEM_ENUMERIC = -5  /* non-finite eigenvalue bound, gamma or shift */
+};
+
+/*
+ * hpfem_plan -- Alg. 2 "Precomputation" on a uniform mesh.
+ *   n_x elements on [a,b] of degree p_x; n_y elements on [c,d] of degree p_y
+ *   (p >= 2: hats plus bubbles W_0..W_{p-2}); omega = w of eq. poisson;
+ *   bc = HPFEM_BC_*; tol = epsilon of Lemma 5.1, 0 < tol < 1.
+ * Builds the 1D operators (closed forms of App. A), the
+ * spectral intervals [lambda_min, lambda_max] of (A_d, M_d) (DESIGN.md
+ * reading R4), gamma, J = ceil(log(16 gamma) log(4/tol)/pi^2), the
+ * Zolotarev shifts p_j > 0, q_j < 0 (reading R5), and factors the
+ * 2J+1 shifted 1D matrices on the device (Alg. 1).  Synchronises
+ * cuda_stream once (to read back the factorisation status).
+ * On success *out receives a plan to be released with hpfem_plan_destroy.
+ */
+int hpfem_plan(int n_x, int p_x, int n_y, int p_y, double a, double b, double c, double d, double omega, int bc,
+               double tol, void* cuda_stream, hpfem_plan_t* out);
+
+/* As hpfem_plan with explicit strictly increasing breakpoints xs[0..n_x],
+ * ys[0..n_y] (host arrays, copied; graded meshes). */
+int hpfem_plan_mesh(const double* xs, int n_x, int p_x, const double* ys, int n_y, int p_y, double omega, int bc,
+                    double tol, void* cuda_stream, hpfem_plan_t* out);
+
+/* Plan summary (host outputs; any pointer may be NULL). */
+int hpfem_plan_info(hpfem_plan_t plan, int* N_x, int* N_y, int* J, double* lam_x /*[2]*/, double* lam_y /*[2]*/,
+                    double* gamma);
+
+/* Host copies of the shifts: p[0..J-1] (used by the y-solves and the
+ * x-applies), q[0..J-1] (x-solves and y-applies), ascending j. */
+int hpfem_plan_shifts(hpfem_plan_t plan, double* p, double* q);
+
+/*
+ * hpfem_solve -- Alg. 2 "Solve": U = W_J C^{-1} with
+ *   W_{j-1/2} = (G - (A_x - p_j M_x) W_{j-1}) (A_y + p_j M_y)^{-1}
+ *   W_j       = (A_x - q_j M_x)^{-1} (G - W_{j-1/2} (A_y + q_j M_y))
+ * (the "plus" form of the listing, reading R6), satisfying the
+ * Lemma 5.1 bound ||V(U* - U)L^T|| <= tol ||V U* L^T||.
+ *   F: device pointer, G of eq. adi:poisson (for a Legendre-coefficient f
+ *      this is hpfem_load(f)), N_x x N_y.   U: device pointer, N_x x N_y.
+ * F and U must not overlap (HPFEM_EINVAL).  F is not modified.
+ */
+int hpfem_solve(hpfem_plan_t plan, const double* F, double* U, void* cuda_stream);
+
+/* As hpfem_solve but running only the first `iters` ADI iterations
+ * (0 <= iters <= J) before the final W C^{-1}; iters = J is hpfem_solve.
+ * Used for truncated-iteration parity at full size. */
+int hpfem_solve_iters(hpfem_plan_t plan, const double* F, double* U, int iters, void* cuda_stream);
+
+/* hpfem_apply -- F = A_x U M_y + M_x U A_y (the operator of eq. adi:poisson,
+ * P:L658-L664).  U, F device pointers, N_x x N_y, must not overlap. */
+int hpfem_apply(hpfem_plan_t plan, const double* U, double* F, void* cuda_stream);
+
+/* hpfem_load -- G = R_x^T M_{P,x} F_leg M_{P,y} R_y.
+ * F_leg: device, ((p_x+1) n_x) x ((p_y+1) n_y) row-major, degree-major /
+ * element-minor (entry [m n_x + e, l n_y + f] multiplies P_m(x) P_l(y) on
+ * element (e, f)).  G: device, N_x x N_y.  Must not overlap. */
+int hpfem_load(hpfem_plan_t plan, const double* F_leg, double* G, void* cuda_stream);
+
+/* Kernel launches enqueued by the last hpfem_* device call of this plan
+ * (for the bench's launch accounting). */
+int hpfem_plan_launches(hpfem_plan_t plan, long long* launches);
+
+/*
+ * Per-kernel timing with CUDA events recorded on the launch stream around
+ * every kernel of subsequent hpfem_solve / hpfem_load / hpfem_apply calls
+ * (bench.py's roofline).  hpfem_plan_profile(plan, capacity) creates
+ * `capacity` events up front (0 disables and frees them).
+ * hpfem_plan_profile_read synchronises on the last event and returns, per
+ * kernel kind k (0 = half-step bubble kernel K2-K4, 1 = hat kernel K5,
+ * 2 = final W C^{-1} kernels, 3 = load K8, 4 = apply K7), the summed
+ * duration ms[k], launch count n[k] and algorithmic HBM bytes bytes[k]
+ * (DESIGN.md "Roofline"), then resets the counters.  Events beyond the
+ * capacity are not recorded (n[] tells).
+ */
+int hpfem_plan_profile(hpfem_plan_t plan, int capacity);
+int hpfem_plan_profile_read(hpfem_plan_t plan, double* ms /*[5]*/, long long* n /*[5]*/, double* bytes /*[5]*/);
+
+void hpfem_plan_destroy(hpfem_plan_t plan);
+
+/* Thread-local message for the last error on this thread ("" if none). */
+const char* hpfem_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPFEM_H_ */

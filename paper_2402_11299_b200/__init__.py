@@ -1,0 +1,231 @@
+"""Thin Python binding of libhpfem_b200.so (the C ABI of include/hpfem.h).
+
+Argument marshalling only: every step of the ADI solve runs in the CUDA
+kernels of csrc/kernels.cu.  There is no CPU fallback -- if the extension is
+missing or no sm_100 device is usable, calls raise.  PyTorch is used only to
+hand over device pointers and the current CUDA stream.
+
+The functions carry the C names (hpfem_plan, hpfem_solve, ...); `Plan` is a
+small RAII convenience around them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhpfem_b200.so")
+
+HPFEM_BC_DIRICHLET = 0
+HPFEM_BC_NEUMANN = 1
+HPFEM_OK, HPFEM_EINVAL, HPFEM_ENOTPD, HPFEM_ECUDA, HPFEM_ENOMEM, HPFEM_ENUMERIC = 0, -1, -2, -3, -4, -5
+_NAMES = {-1: "EINVAL", -2: "ENOTPD", -3: "ECUDA", -4: "ENOMEM", -5: "ENUMERIC"}
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+_vp = ctypes.c_void_p
+_i, _d = ctypes.c_int, ctypes.c_double
+_LIB = None
+
+
+def _load():
+    """Load the CUDA library (lazily, so the build module can be imported
+    before it exists).  Missing library = loud ImportError, never a fallback."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2402_11299_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    L.hpfem_plan.argtypes = [_i, _i, _i, _i, _d, _d, _d, _d, _d, _i, _d, _vp, ctypes.POINTER(_vp)]
+    L.hpfem_plan_mesh.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _d, _vp, ctypes.POINTER(_vp)]
+    L.hpfem_plan_info.argtypes = [_vp, _ip, _ip, _ip, _dp, _dp, _dp]
+    L.hpfem_plan_shifts.argtypes = [_vp, _dp, _dp]
+    L.hpfem_solve.argtypes = [_vp, _vp, _vp, _vp]
+    L.hpfem_solve_iters.argtypes = [_vp, _vp, _vp, _i, _vp]
+    L.hpfem_apply.argtypes = [_vp, _vp, _vp, _vp]
+    L.hpfem_load.argtypes = [_vp, _vp, _vp, _vp]
+    L.hpfem_plan_launches.argtypes = [_vp, ctypes.POINTER(ctypes.c_longlong)]
+    L.hpfem_plan_profile.argtypes = [_vp, _i]
+    L.hpfem_plan_profile_read.argtypes = [_vp, _dp, ctypes.POINTER(ctypes.c_longlong), _dp]
+    L.hpfem_plan_destroy.argtypes = [_vp]
+    L.hpfem_plan_destroy.restype = None
+    L.hpfem_last_error.restype = ctypes.c_char_p
+    for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
+              "hpfem_solve_iters", "hpfem_apply", "hpfem_load", "hpfem_plan_launches", "hpfem_plan_profile",
+              "hpfem_plan_profile_read"):
+        getattr(L, f).restype = _i
+    _LIB = L
+    return L
+
+
+EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
+           "hpfem_solve_iters", "hpfem_apply", "hpfem_load", "hpfem_plan_launches", "hpfem_plan_profile",
+           "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error")
+
+
+class HpfemError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"HPFEM_{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def hpfem_last_error() -> str:
+    return _load().hpfem_last_error().decode()
+
+
+def _check(rc: int):
+    if rc != HPFEM_OK:
+        raise HpfemError(rc, hpfem_last_error())
+
+
+def _ptr(x) -> int:
+    """Device pointer of a CUDA float64 contiguous tensor (or a raw int)."""
+    if isinstance(x, int):
+        return x
+    if not x.is_cuda:
+        raise ValueError("expected a CUDA tensor (the C ABI takes device pointers)")
+    if not x.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    import torch
+    if x.dtype != torch.float64:
+        raise ValueError("expected float64")
+    return x.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def hpfem_plan(n_x, p_x, n_y, p_y, a, b, c, d, omega, bc, tol, stream=None) -> int:
+    h = _vp()
+    _check(_load().hpfem_plan(n_x, p_x, n_y, p_y, a, b, c, d, omega, bc, tol, _stream(stream), ctypes.byref(h)))
+    return h.value
+
+
+def hpfem_plan_mesh(xs, p_x, ys, p_y, omega, bc, tol, stream=None) -> int:
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    ys = np.ascontiguousarray(ys, dtype=np.float64)
+    h = _vp()
+    _check(_load().hpfem_plan_mesh(xs.ctypes.data_as(_dp), xs.size - 1, p_x, ys.ctypes.data_as(_dp), ys.size - 1, p_y,
+                                omega, bc, tol, _stream(stream), ctypes.byref(h)))
+    return h.value
+
+
+def hpfem_plan_info(plan: int) -> dict:
+    Nx, Ny, J = _i(), _i(), _i()
+    lx, ly = (ctypes.c_double * 2)(), (ctypes.c_double * 2)()
+    g = _d()
+    _check(_load().hpfem_plan_info(plan, ctypes.byref(Nx), ctypes.byref(Ny), ctypes.byref(J), lx, ly, ctypes.byref(g)))
+    return dict(Nx=Nx.value, Ny=Ny.value, J=J.value, lam_x=np.array(lx[:]), lam_y=np.array(ly[:]), gamma=g.value)
+
+
+def hpfem_plan_shifts(plan: int):
+    J = hpfem_plan_info(plan)["J"]
+    p, q = np.empty(J), np.empty(J)
+    _check(_load().hpfem_plan_shifts(plan, p.ctypes.data_as(_dp), q.ctypes.data_as(_dp)))
+    return p, q
+
+
+def hpfem_solve(plan: int, F, U, stream=None):
+    _check(_load().hpfem_solve(plan, _ptr(F), _ptr(U), _stream(stream)))
+
+
+def hpfem_solve_iters(plan: int, F, U, iters: int, stream=None):
+    _check(_load().hpfem_solve_iters(plan, _ptr(F), _ptr(U), iters, _stream(stream)))
+
+
+def hpfem_apply(plan: int, U, F, stream=None):
+    _check(_load().hpfem_apply(plan, _ptr(U), _ptr(F), _stream(stream)))
+
+
+def hpfem_load(plan: int, F_leg, G, stream=None):
+    _check(_load().hpfem_load(plan, _ptr(F_leg), _ptr(G), _stream(stream)))
+
+
+def hpfem_plan_launches(plan: int) -> int:
+    n = ctypes.c_longlong(0)
+    _check(_load().hpfem_plan_launches(plan, ctypes.byref(n)))
+    return n.value
+
+
+KINDS = ("halfstep_bubbles", "halfstep_hats", "final", "load", "apply")
+
+
+def hpfem_plan_profile(plan: int, capacity: int):
+    _check(_load().hpfem_plan_profile(plan, capacity))
+
+
+def hpfem_plan_profile_read(plan: int) -> dict:
+    ms = (ctypes.c_double * 5)()
+    n = (ctypes.c_longlong * 5)()
+    by = (ctypes.c_double * 5)()
+    _check(_load().hpfem_plan_profile_read(plan, ms, n, by))
+    return {k: dict(ms=ms[i], launches=n[i], bytes=by[i]) for i, k in enumerate(KINDS)}
+
+
+def hpfem_plan_destroy(plan: int):
+    if plan:
+        _load().hpfem_plan_destroy(plan)
+
+
+class Plan:
+    """RAII wrapper: Plan(xs, px, ys, py, omega, bc, tol) or Plan.uniform(...)."""
+
+    def __init__(self, xs, px, ys, py, omega, bc, tol, stream=None):
+        self.handle = hpfem_plan_mesh(xs, px, ys, py, omega, bc, tol, stream)
+        info = hpfem_plan_info(self.handle)
+        self.__dict__.update(info)
+        self.px, self.py, self.bc, self.omega, self.tol = px, py, bc, omega, tol
+        self.nx, self.ny = len(xs) - 1, len(ys) - 1
+
+    @classmethod
+    def uniform(cls, n_x, p_x, n_y, p_y, a, b, c, d, omega, bc, tol, stream=None):
+        obj = cls.__new__(cls)
+        obj.handle = hpfem_plan(n_x, p_x, n_y, p_y, a, b, c, d, omega, bc, tol, stream)
+        obj.__dict__.update(hpfem_plan_info(obj.handle))
+        obj.px, obj.py, obj.bc, obj.omega, obj.tol, obj.nx, obj.ny = p_x, p_y, bc, omega, tol, n_x, n_y
+        return obj
+
+    def shifts(self):
+        return hpfem_plan_shifts(self.handle)
+
+    def solve(self, F, U, stream=None, iters=None):
+        if iters is None:
+            hpfem_solve(self.handle, F, U, stream)
+        else:
+            hpfem_solve_iters(self.handle, F, U, iters, stream)
+
+    def apply(self, U, F, stream=None):
+        hpfem_apply(self.handle, U, F, stream)
+
+    def load(self, F_leg, G, stream=None):
+        hpfem_load(self.handle, F_leg, G, stream)
+
+    def profile(self, capacity: int):
+        hpfem_plan_profile(self.handle, capacity)
+
+    def profile_read(self) -> dict:
+        return hpfem_plan_profile_read(self.handle)
+
+    def launches(self) -> int:
+        return hpfem_plan_launches(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            hpfem_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,545 @@
+/*
+ * kernels.cu -- fp64 device kernels of the ADI hp-FEM solve for sm_100a.
+ *
+ * The path is banded / tridiagonal recurrence work with ~0.65 flop per byte
+ * (DESIGN.md "Roofline"), so it is bound by HBM bandwidth and latency, not
+ * by any tensor pipe: no tcgen05 / TMEM here by design.
+ *
+ *   K1  k_factor_chains / k_factor_hats  Alg. 1 for a batch of
+ *       shifted operators S = kap K + sig M: per (shift, element, parity)
+ *       bubble chain reverse Cholesky, the static-condensation vectors
+ *       v = D_e^{-1} B^T e_h, and the hat Schur complement A0 - B D^{-1} B^T
+ *       factored by reverse Cholesky.
+ *   K2+K3+K4  k_bubbles<DIR,CL>: one pass over all lines of a half-step of
+ *       Alg. 2: the cross-line sparse apply of the other
+ *       direction is evaluated on the loads (K3 fused into K2/K4), then the
+ *       element-local bubble solve z = D_e^{-1} r_b runs in registers
+ *       (Cor. 4.3 P:L600-L614 in static-condensation form).
+ *   K5  k_hats<DIR>: per line, hat RHS r_h - B z and the hat tridiagonal
+ *       solve; the bubble correction x_b = z - v x_h is deferred into the
+ *       consumer's loads (the next half-step's stencil, or K6).
+ *   K6  k_correct_rows: materialises U = W_J C^{-1}.
+ *   K7  k_apply2d: F = A_x U M_y + M_x U A_y.     K8 k_load2d: G = R^T M_P F M_P R.
+ */
+#include <cstdint>
+
+#include "hpfem_internal.h"
+#include "ops1d.h"
+
+namespace hpfem {
+
+/* ------------------------------------------------------------------ */
+/* K1: factorisation of a batch of shifted 1D operators               */
+/* ------------------------------------------------------------------ */
+__device__ void report(int* err, int code, int set, int where, int k) {
+  if (atomicCAS(err, 0, code) == 0) {
+    err[1] = set;
+    err[2] = where;
+    err[3] = k;
+  }
+}
+
+__global__ void k_factor_chains(DirDev d, const double* __restrict__ kap, const double* __restrict__ sig, int nsets,
+                                double* __restrict__ fac, size_t stride, int* err) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= nsets * d.n * 2) return;
+  const int e = tid % d.n;
+  const int pi = (tid / d.n) & 1;
+  const int s = tid / (2 * d.n);
+  const int m = chain_len(d.p, pi);
+  if (m == 0) return;
+  const double K = kap[s], S = sig[s], delta = d.delta[e];
+  double* base = fac + (size_t)s * stride;
+  double* il = base;
+  double* g = base + d.nb;
+  double* vL = base + 2 * (size_t)d.nb;
+  double* vR = base + 3 * (size_t)d.nb;
+  // chain T = L^T L, L lower bidiagonal (diag l_c, sub g_c = L[c+1,c]),
+  // bottom-up (reverse Cholesky): l_{m-1} = sqrt(a_{m-1});
+  // g_c = b_c / l_{c+1}; l_c = sqrt(a_c - g_c^2)
+  double lnext = 0.0;
+  for (int c = m - 1; c >= 0; --c) {
+    const int k = pi + 2 * c;
+    const int b = k * d.n + e;
+    double a = s_bub_diag(K, S, delta, k);
+    double gc = 0.0;
+    if (c < m - 1) {
+      gc = s_bub_off(S, delta, k) / lnext;
+      a -= gc * gc;
+    }
+    if (!(a > 0.0) || !isfinite(a)) {
+      report(err, 1, s, e, k);
+      a = 1.0;
+    }
+    const double l = sqrt(a);
+    il[b] = 1.0 / l;
+    g[b] = gc;
+    lnext = l;
+  }
+  // v_side = T^{-1} (beta e_0): the chain-first bubble is the only one
+  // coupled to the hats (W_0 / W_1, ops1d.h)
+  for (int side = 0; side < 2; ++side) {
+    const int h = hat_of_node(e + side, d.n, d.bc);
+    const double beta = (h >= 0) ? s_hat_bub(S, delta, side, pi) : 0.0;
+    double* v = side ? vR : vL;
+    const int b0 = pi * d.n + e;
+    double z = beta * il[b0] * il[b0];
+    v[b0] = z;
+    int bprev = b0;
+    for (int c = 1; c < m; ++c) {
+      const int b = (pi + 2 * c) * d.n + e;
+      z = -g[bprev] * z * il[b];
+      v[b] = z;
+      bprev = b;
+    }
+  }
+}
+
+__device__ double schur_elem(const DirDev& d, double S, const double* vv, int e, int side_row) {
+  // (B D^{-1} B^T)[h_row, h_col] restricted to element e: sum_k B[h_row, W_k] v_col[k]
+  const double delta = d.delta[e];
+  double acc = s_hat_bub(S, delta, side_row, 0) * vv[e];
+  if (d.p - 2 >= 1) acc += s_hat_bub(S, delta, side_row, 1) * vv[d.n + e];
+  return acc;
+}
+
+__global__ void k_factor_hats(DirDev d, const double* __restrict__ kap, const double* __restrict__ sig, int nsets,
+                              double* __restrict__ fac, size_t stride, int* err) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nsets || d.nh == 0) return;
+  const double K = kap[s], S = sig[s];
+  double* base = fac + (size_t)s * stride;
+  const double* vL = base + 2 * (size_t)d.nb;
+  const double* vR = base + 3 * (size_t)d.nb;
+  double* ilh = base + 4 * (size_t)d.nb;
+  double* gh = ilh + d.nh;
+  double lnext = 0.0;
+  for (int t = d.nh - 1; t >= 0; --t) {
+    const int node = node_of_hat(t, d.bc);
+    const int eL = node - 1, eR = node;
+    double diag = 0.0;
+    if (eL >= 0) diag += s_hat_diag_elem(K, S, d.delta[eL]) - schur_elem(d, S, vR, eL, 1);
+    if (eR <= d.n - 1) diag += s_hat_diag_elem(K, S, d.delta[eR]) - schur_elem(d, S, vL, eR, 0);
+    double gc = 0.0;
+    if (t < d.nh - 1) {
+      // A~0(t, t+1): element eR lies between the two nodes; t is its left hat
+      const double off = s_hat_off_elem(K, S, d.delta[eR]) - schur_elem(d, S, vR, eR, 0);
+      gc = off / lnext;
+      diag -= gc * gc;
+    }
+    if (!(diag > 0.0) || !isfinite(diag)) {
+      report(err, 2, s, t, -1);
+      diag = 1.0;
+    }
+    const double l = sqrt(diag);
+    ilh[t] = 1.0 / l;
+    gh[t] = gc;
+    lnext = l;
+  }
+}
+
+cudaError_t launch_factor(const DirDev& d, const double* kap, const double* sig, int nsets, double* fac,
+                          size_t stride, int* err, cudaStream_t st) {
+  const int nthr = nsets * d.n * 2;
+  k_factor_chains<<<(nthr + 127) / 128, 128, 0, st>>>(d, kap, sig, nsets, fac, stride, err);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_factor_hats<<<(nsets + 31) / 32, 32, 0, st>>>(d, kap, sig, nsets, fac, stride, err);
+  return cudaGetLastError();
+}
+
+/* ------------------------------------------------------------------ */
+/* Cross-line stencil: row l (in direction o) of  -S_o Corr_o  (apply) */
+/* or +Corr_o (final), as 7 fixed slots so it stays in registers.      */
+/* Bubble row (k,e): [l, l-2n, l+2n, hL(e), hR(e), -, -]               */
+/* Hat row t      : [t, t-1, t+1, (0,eL), (1,eL), (0,eR), (1,eR)]      */
+/* ------------------------------------------------------------------ */
+struct Stencil {
+  int idx[7];
+  double w[7];
+};
+
+__device__ __forceinline__ void stencil_build(const DirDev& o, int l, int mode, double kap, double tau,
+                                              const double* __restrict__ cvL, const double* __restrict__ cvR,
+                                              Stencil& st) {
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    st.idx[q] = -1;
+    st.w[q] = 0.0;
+  }
+  if (mode == ST_NONE) return;
+  const int n = o.n, nh = o.nh;
+  if (l >= nh) {
+    const int b = l - nh;
+    const int k = b / n;
+    const int e = b - k * n;
+    const int hL = hat_of_node(e, n, o.bc), hR = hat_of_node(e + 1, n, o.bc);
+    if (mode == ST_CORR) {
+      st.idx[0] = l;
+      st.w[0] = 1.0;
+      if (hL >= 0 && cvL) { st.idx[3] = hL; st.w[3] = -cvL[b]; }
+      if (hR >= 0 && cvR) { st.idx[4] = hR; st.w[4] = -cvR[b]; }
+      return;
+    }
+    const double dl = o.delta[e];
+    const bool hm = k >= 2, hp = k + 2 <= o.p - 2;
+    const double sd = s_bub_diag(kap, tau, dl, k);
+    const double sm = hm ? s_bub_off(tau, dl, k - 2) : 0.0;
+    const double sp = hp ? s_bub_off(tau, dl, k) : 0.0;
+    double cL = s_hat_bub(tau, dl, 0, k), cR = s_hat_bub(tau, dl, 1, k);
+    if (cvL) {
+      cL -= sd * cvL[b];
+      if (hm) cL -= sm * cvL[b - 2 * n];
+      if (hp) cL -= sp * cvL[b + 2 * n];
+    }
+    if (cvR) {
+      cR -= sd * cvR[b];
+      if (hm) cR -= sm * cvR[b - 2 * n];
+      if (hp) cR -= sp * cvR[b + 2 * n];
+    }
+    st.idx[0] = l; st.w[0] = -sd;
+    if (hm) { st.idx[1] = l - 2 * n; st.w[1] = -sm; }
+    if (hp) { st.idx[2] = l + 2 * n; st.w[2] = -sp; }
+    if (hL >= 0) { st.idx[3] = hL; st.w[3] = -cL; }
+    if (hR >= 0) { st.idx[4] = hR; st.w[4] = -cR; }
+  } else {
+    const int t = l;
+    if (mode == ST_CORR) {
+      st.idx[0] = t;
+      st.w[0] = 1.0;
+      return;
+    }
+    const int node = node_of_hat(t, o.bc);
+    const int eL = node - 1, eR = node;
+    const bool k1 = o.p - 2 >= 1;
+    double ctt = 0.0, ctm = 0.0, ctp = 0.0;
+    bool has_m = false, has_p = false;
+    if (eL >= 0) {
+      const double dl = o.delta[eL];
+      ctt += s_hat_diag_elem(kap, tau, dl);
+      has_m = hat_of_node(node - 1, n, o.bc) >= 0;
+      if (has_m) ctm += s_hat_off_elem(kap, tau, dl);
+      const double s0 = s_hat_bub(tau, dl, 1, 0), s1 = k1 ? s_hat_bub(tau, dl, 1, 1) : 0.0;
+      st.idx[3] = nh + eL; st.w[3] = -s0;
+      if (k1) { st.idx[4] = nh + n + eL; st.w[4] = -s1; }
+      if (cvR) ctt -= s0 * cvR[eL] + (k1 ? s1 * cvR[n + eL] : 0.0);
+      if (cvL && has_m) ctm -= s0 * cvL[eL] + (k1 ? s1 * cvL[n + eL] : 0.0);
+    }
+    if (eR <= n - 1) {
+      const double dr = o.delta[eR];
+      ctt += s_hat_diag_elem(kap, tau, dr);
+      has_p = hat_of_node(node + 1, n, o.bc) >= 0;
+      if (has_p) ctp += s_hat_off_elem(kap, tau, dr);
+      const double s0 = s_hat_bub(tau, dr, 0, 0), s1 = k1 ? s_hat_bub(tau, dr, 0, 1) : 0.0;
+      st.idx[5] = nh + eR; st.w[5] = -s0;
+      if (k1) { st.idx[6] = nh + n + eR; st.w[6] = -s1; }
+      if (cvL) ctt -= s0 * cvL[eR] + (k1 ? s1 * cvL[n + eR] : 0.0);
+      if (cvR && has_p) ctp -= s0 * cvR[eR] + (k1 ? s1 * cvR[n + eR] : 0.0);
+    }
+    st.idx[0] = t; st.w[0] = -ctt;
+    if (has_m) { st.idx[1] = t - 1; st.w[1] = -ctm; }
+    if (has_p) { st.idx[2] = t + 1; st.w[2] = -ctp; }
+  }
+}
+
+/* address of (line l, dof d) for a solve along DIR */
+template <int DIR>
+__device__ __forceinline__ size_t addr(int l, int d, int ld) {
+  return DIR == 0 ? (size_t)d * ld + l : (size_t)l * ld + d;
+}
+
+/* r(l, d) = alphaG G(l,d) + sum_q w_q Xp(idx_q, d) */
+template <int DIR>
+__device__ __forceinline__ double rhs_at(const StepParams& P, const Stencil& st, int l, int d) {
+  double acc = 0.0;
+  if (P.alphaG != 0.0) acc = P.alphaG * __ldg(P.G + addr<DIR>(l, d, P.ld));
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+    if (st.idx[q] >= 0) acc += st.w[q] * __ldg(P.Xp + addr<DIR>(st.idx[q], d, P.ld));
+  return acc;
+}
+
+template <int DIR>
+__device__ __forceinline__ bool thread_coords(const StepParams& P, int& l, int& e, int& pi) {
+  const int n = P.s.n;
+  if (DIR == 0) {
+    l = blockIdx.x * blockDim.x + threadIdx.x;
+    e = blockIdx.y % n;
+    pi = blockIdx.y / n;
+  } else {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    e = (int)(idx % n);
+    pi = (int)((idx / n) & 1);
+    l = (int)(idx / (2 * n));
+  }
+  return l < P.o.N;
+}
+
+/* K2/K3/K4: fused apply + element-local bubble chain solve, chain in registers */
+template <int DIR, int CL>
+__global__ void __launch_bounds__(128) k_bubbles(StepParams P) {
+  int l, e, pi;
+  if (!thread_coords<DIR>(P, l, e, pi)) return;
+  const DirDev& s = P.s;
+  const int m = chain_len(s.p, pi);
+  if (m == 0) return;
+  Stencil st;
+  stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+  double r[CL];
+#pragma unroll
+  for (int c = 0; c < CL; ++c)
+    if (c < m) r[c] = rhs_at<DIR>(P, st, l, s.nh + (pi + 2 * c) * s.n + e);
+  // L^T y = r (descending), then L z = y (ascending): z = D_e^{-1} r on this chain
+  const double* __restrict__ il = P.f.il;
+  const double* __restrict__ g = P.f.g;
+  double y = 0.0;
+#pragma unroll
+  for (int c = CL - 1; c >= 0; --c)
+    if (c < m) {
+      const int b = (pi + 2 * c) * s.n + e;
+      y = (r[c] - __ldg(g + b) * y) * __ldg(il + b);
+      r[c] = y;
+    }
+  double z = 0.0, gp = 0.0;
+#pragma unroll
+  for (int c = 0; c < CL; ++c)
+    if (c < m) {
+      const int b = (pi + 2 * c) * s.n + e;
+      z = (r[c] - gp * z) * __ldg(il + b);
+      gp = __ldg(g + b);
+      P.out[addr<DIR>(l, s.nh + b, P.ld)] = z;
+    }
+}
+
+/* long chains (> 64): y staged through the output array (L2 round trip) */
+template <int DIR>
+__global__ void __launch_bounds__(128) k_bubbles_long(StepParams P) {
+  int l, e, pi;
+  if (!thread_coords<DIR>(P, l, e, pi)) return;
+  const DirDev& s = P.s;
+  const int m = chain_len(s.p, pi);
+  if (m == 0) return;
+  Stencil st;
+  stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+  const double* __restrict__ il = P.f.il;
+  const double* __restrict__ g = P.f.g;
+  double y = 0.0;
+#pragma unroll 8
+  for (int c = m - 1; c >= 0; --c) {
+    const int b = (pi + 2 * c) * s.n + e;
+    const double r = rhs_at<DIR>(P, st, l, s.nh + b);
+    y = (r - __ldg(g + b) * y) * __ldg(il + b);
+    P.out[addr<DIR>(l, s.nh + b, P.ld)] = y;
+  }
+  double z = 0.0, gp = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < m; ++c) {
+    const int b = (pi + 2 * c) * s.n + e;
+    double* o = P.out + addr<DIR>(l, s.nh + b, P.ld);
+    z = (*o - gp * z) * __ldg(il + b);
+    gp = __ldg(g + b);
+    *o = z;
+  }
+}
+
+/* K5: per line, hat RHS r_h - B z and the hat tridiagonal solve */
+template <int DIR>
+__global__ void __launch_bounds__(128) k_hats(StepParams P) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= P.o.N) return;
+  const DirDev& s = P.s;
+  if (s.nh == 0) return;
+  Stencil st;
+  stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+  const double S = P.f.sig;
+  const bool k1 = s.p - 2 >= 1;
+  double y = 0.0;
+  for (int t = s.nh - 1; t >= 0; --t) {
+    double rh = rhs_at<DIR>(P, st, l, t);
+    const int node = node_of_hat(t, s.bc);
+    const int eL = node - 1, eR = node;
+    if (eL >= 0) {
+      const double dl = s.delta[eL];
+      rh -= s_hat_bub(S, dl, 1, 0) * P.out[addr<DIR>(l, s.nh + eL, P.ld)];
+      if (k1) rh -= s_hat_bub(S, dl, 1, 1) * P.out[addr<DIR>(l, s.nh + s.n + eL, P.ld)];
+    }
+    if (eR <= s.n - 1) {
+      const double dr = s.delta[eR];
+      rh -= s_hat_bub(S, dr, 0, 0) * P.out[addr<DIR>(l, s.nh + eR, P.ld)];
+      if (k1) rh -= s_hat_bub(S, dr, 0, 1) * P.out[addr<DIR>(l, s.nh + s.n + eR, P.ld)];
+    }
+    y = (rh - __ldg(P.f.gh + t) * y) * __ldg(P.f.ilh + t);
+    P.out[addr<DIR>(l, t, P.ld)] = y;
+  }
+  double x = 0.0, gp = 0.0;
+  for (int t = 0; t < s.nh; ++t) {
+    double* o = P.out + addr<DIR>(l, t, P.ld);
+    x = (*o - gp * x) * __ldg(P.f.ilh + t);
+    gp = __ldg(P.f.gh + t);
+    *o = x;
+  }
+}
+
+template <int DIR, int CL>
+static cudaError_t launch_bub(const StepParams& P, cudaStream_t st) {
+  if (DIR == 0) {
+    dim3 grid((P.o.N + 127) / 128, P.s.n * 2);
+    k_bubbles<DIR, CL><<<grid, 128, 0, st>>>(P);
+  } else {
+    const long long nthr = (long long)P.o.N * 2 * P.s.n;
+    k_bubbles<DIR, CL><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(P);
+  }
+  return cudaGetLastError();
+}
+
+template <int DIR>
+static cudaError_t launch_bub_dir(const StepParams& P, cudaStream_t st) {
+  const int m = chain_len(P.s.p, 0);
+  if (m <= 4) return launch_bub<DIR, 4>(P, st);
+  if (m <= 8) return launch_bub<DIR, 8>(P, st);
+  if (m <= 16) return launch_bub<DIR, 16>(P, st);
+  if (m <= 32) return launch_bub<DIR, 32>(P, st);
+  if (m <= 64) return launch_bub<DIR, 64>(P, st);
+  if (DIR == 0) {
+    dim3 grid((P.o.N + 127) / 128, P.s.n * 2);
+    k_bubbles_long<DIR><<<grid, 128, 0, st>>>(P);
+  } else {
+    const long long nthr = (long long)P.o.N * 2 * P.s.n;
+    k_bubbles_long<DIR><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(P);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st) {
+  return P.dir == 0 ? launch_bub_dir<0>(P, st) : launch_bub_dir<1>(P, st);
+}
+
+cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st) {
+  if (P.s.nh == 0) return cudaSuccess;
+  const unsigned grid = (P.o.N + 127) / 128;
+  if (P.dir == 0)
+    k_hats<0><<<grid, 128, 0, st>>>(P);
+  else
+    k_hats<1><<<grid, 128, 0, st>>>(P);
+  return cudaGetLastError();
+}
+
+/* K6: U(i, b) = z(i, b) - vL(b) x_h(i, hL) - vR(b) x_h(i, hR) along rows */
+__global__ void k_correct_rows(DirDev y, int Nx, const double* __restrict__ vL, const double* __restrict__ vR,
+                               double* __restrict__ U) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (b >= y.nb || i >= Nx) return;
+  const int e = b % y.n;
+  const int hL = hat_of_node(e, y.n, y.bc), hR = hat_of_node(e + 1, y.n, y.bc);
+  double* row = U + (size_t)i * y.N;
+  double v = row[y.nh + b];
+  if (hL >= 0) v -= __ldg(vL + b) * row[hL];
+  if (hR >= 0) v -= __ldg(vR + b) * row[hR];
+  row[y.nh + b] = v;
+}
+
+cudaError_t launch_correct_rows(const DirDev& y, int Nx, const double* vL, const double* vR, double* U,
+                                cudaStream_t st) {
+  dim3 grid((y.nb + 255) / 256, Nx);
+  k_correct_rows<<<grid, 256, 0, st>>>(y, Nx, vL, vR, U);
+  return cudaGetLastError();
+}
+
+/* K7: F = A_x U M_y + M_x U A_y, A = K + (w^2/2) M */
+__global__ void __launch_bounds__(128) k_apply2d(DirDev x, DirDev y, double half_w2, const double* __restrict__ U,
+                                                  double* __restrict__ F) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= y.N) return;
+  Stencil ax, mx, ay, my;  // weights are -(row entries)
+  stencil_build(x, i, ST_APPLY, 1.0, half_w2, nullptr, nullptr, ax);
+  stencil_build(x, i, ST_APPLY, 0.0, 1.0, nullptr, nullptr, mx);
+  stencil_build(y, j, ST_APPLY, 1.0, half_w2, nullptr, nullptr, ay);
+  stencil_build(y, j, ST_APPLY, 0.0, 1.0, nullptr, nullptr, my);
+  double acc = 0.0;
+#pragma unroll
+  for (int a = 0; a < 7; ++a) {
+    if (ax.idx[a] < 0) continue;
+    const double* row = U + (size_t)ax.idx[a] * y.N;
+    double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+    for (int b = 0; b < 7; ++b) {
+      if (my.idx[b] < 0) continue;
+      const double u = __ldg(row + my.idx[b]);
+      t1 += my.w[b] * u;
+      t2 += ay.w[b] * u;
+    }
+    acc += ax.w[a] * t1 + mx.w[a] * t2;
+  }
+  F[(size_t)i * y.N + j] = acc;
+}
+
+cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const double* U, double* F,
+                           cudaStream_t st) {
+  dim3 grid((y.N + 127) / 128, x.N);
+  k_apply2d<<<grid, 128, 0, st>>>(x, y, 0.5 * omega * omega, U, F);
+  return cudaGetLastError();
+}
+
+/* K8 helper: Legendre sources of dof l: (M_P R)[(m,e), l] (App. A) */
+__device__ __forceinline__ int load_sources(const DirDev& o, int l, int* r, double* w) {
+  const int n = o.n;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    r[q] = -1;
+    w[q] = 0.0;
+  }
+  if (l >= o.nh) {
+    const int b = l - o.nh, k = b / n, e = b - k * n;
+    const double d = o.delta[e];
+    r[0] = k * n + e;
+    w[0] = (d / (2.0 * k + 1.0)) * (1.0 / (2.0 * k + 3.0));
+    r[1] = (k + 2) * n + e;
+    w[1] = (d / (2.0 * k + 5.0)) * (-1.0 / (2.0 * k + 3.0));
+  } else {
+    const int node = node_of_hat(l, o.bc), eL = node - 1, eR = node;
+    if (eL >= 0) {  // right hat of eL: (1+t)/2 = P0/2 + P1/2
+      const double d = o.delta[eL];
+      r[0] = eL; w[0] = d * 0.5;
+      r[1] = n + eL; w[1] = (d / 3.0) * 0.5;
+    }
+    if (eR <= n - 1) {  // left hat of eR: (1-t)/2 = P0/2 - P1/2
+      const double d = o.delta[eR];
+      r[2] = eR; w[2] = d * 0.5;
+      r[3] = n + eR; w[3] = (d / 3.0) * -0.5;
+    }
+  }
+  return 0;
+}
+
+__global__ void __launch_bounds__(128) k_load2d(DirDev x, DirDev y, const double* __restrict__ Fl,
+                                                 double* __restrict__ G) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= y.N) return;
+  int rx[4], ry[4];
+  double wx[4], wy[4];
+  load_sources(x, i, rx, wx);
+  load_sources(y, j, ry, wy);
+  const size_t ldl = (size_t)(y.p + 1) * y.n;
+  double acc = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    if (rx[a] < 0) continue;
+    double t = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (ry[b] >= 0) t += wy[b] * __ldg(Fl + (size_t)rx[a] * ldl + ry[b]);
+    acc += wx[a] * t;
+  }
+  G[(size_t)i * y.N + j] = acc;
+}
+
+cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st) {
+  dim3 grid((y.N + 127) / 128, x.N);
+  k_load2d<<<grid, 128, 0, st>>>(x, y, Fleg, G);
+  return cudaGetLastError();
+}
+
+}  // namespace hpfem

@@ -1,0 +1,658 @@
+/*
+ * plan.cpp -- host plan and C ABI (include/hpfem.h) of the B200 ADI hp-FEM
+ * solver.  Compiled with g++ (binary128 shift arithmetic needs libquadmath);
+ * all array work is enqueued as the device kernels of kernels.cu.
+ *
+ * Plan (Alg. 2 "Precomputation"):
+ *   1. element widths and closed-form 1D entries (ops1d.h, App. A);
+ *   2. spectral interval of (A_d, M_d), A_d = K_d + w^2/2 M_d:
+ *      lambda_min closed form, lambda_max by bisection on "sigma M - A is
+ *      SPD" with the reverse Cholesky of Alg. 1 as the test (R4;
+ *      replaces the Crawford eigensolver of P:L689);
+ *   3. gamma, J and Zolotarev shifts in binary128 (R5);
+ *   4. the 2J+1 shifted factorisations on the device (K1).
+ */
+#include <quadmath.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hpfem.h"
+#include "hpfem_internal.h"
+#include "ops1d.h"
+
+using namespace hpfem;
+
+namespace {
+
+thread_local std::string t_err;
+
+int set_err(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+
+int cuda_err(cudaError_t e, const char* where) {
+  return set_err(HPFEM_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+/* host view of one direction */
+struct DirHost {
+  int n = 0, p = 0, bc = 0, nh = 0, N = 0, nb = 0;
+  std::vector<double> xs, delta;
+};
+
+DirHost make_dir(const double* xs, int n, int p, int bc) {
+  DirHost d;
+  d.n = n;
+  d.p = p;
+  d.bc = bc;
+  d.nh = n_hats(n, bc);
+  d.nb = (p - 1) * n;
+  d.N = d.nh + d.nb;
+  d.xs.assign(xs, xs + n + 1);
+  d.delta.resize(n);
+  for (int e = 0; e < n; ++e) d.delta[e] = xs[e + 1] - xs[e];
+  return d;
+}
+
+/* Host SPD test of S = kap K + sig M by the same chain / Schur-complement
+ * reverse Cholesky the device factor kernel runs (Alg. 1). */
+bool spd_host(const DirHost& d, double kap, double sig) {
+  const int n = d.n;
+  std::vector<double> il(d.nb), g(d.nb), vL(d.nb), vR(d.nb);
+  for (int e = 0; e < n; ++e) {
+    const double dl = d.delta[e];
+    for (int pi = 0; pi < 2; ++pi) {
+      const int m = chain_len(d.p, pi);
+      double lnext = 0.0;
+      for (int c = m - 1; c >= 0; --c) {
+        const int k = pi + 2 * c, b = k * n + e;
+        double a = s_bub_diag(kap, sig, dl, k), gc = 0.0;
+        if (c < m - 1) {
+          gc = s_bub_off(sig, dl, k) / lnext;
+          a -= gc * gc;
+        }
+        if (!(a > 0.0) || !std::isfinite(a)) return false;
+        const double l = std::sqrt(a);
+        il[b] = 1.0 / l;
+        g[b] = gc;
+        lnext = l;
+      }
+      for (int side = 0; side < 2 && m > 0; ++side) {
+        const int h = hat_of_node(e + side, n, d.bc);
+        const double beta = h >= 0 ? s_hat_bub(sig, dl, side, pi) : 0.0;
+        std::vector<double>& v = side ? vR : vL;
+        const int b0 = pi * n + e;
+        double z = beta * il[b0] * il[b0];
+        v[b0] = z;
+        int bp = b0;
+        for (int c = 1; c < m; ++c) {
+          const int b = (pi + 2 * c) * n + e;
+          z = -g[bp] * z * il[b];
+          v[b] = z;
+          bp = b;
+        }
+      }
+    }
+  }
+  auto schur = [&](const std::vector<double>& vv, int e, int side) {
+    double acc = s_hat_bub(sig, d.delta[e], side, 0) * vv[e];
+    if (d.p - 2 >= 1) acc += s_hat_bub(sig, d.delta[e], side, 1) * vv[n + e];
+    return acc;
+  };
+  double lnext = 0.0;
+  for (int t = d.nh - 1; t >= 0; --t) {
+    const int node = node_of_hat(t, d.bc), eL = node - 1, eR = node;
+    double diag = 0.0;
+    if (eL >= 0) diag += s_hat_diag_elem(kap, sig, d.delta[eL]) - schur(vR, eL, 1);
+    if (eR <= n - 1) diag += s_hat_diag_elem(kap, sig, d.delta[eR]) - schur(vL, eR, 0);
+    if (t < d.nh - 1) {
+      const double gc = (s_hat_off_elem(kap, sig, d.delta[eR]) - schur(vR, eR, 0)) / lnext;
+      diag -= gc * gc;
+    }
+    if (!(diag > 0.0) || !std::isfinite(diag)) return false;
+    lnext = std::sqrt(diag);
+  }
+  return true;
+}
+
+/* [lambda_min, lambda_max] of (A, M), A = K + w^2/2 M (reading R4). */
+void spectral_interval(const DirHost& d, double omega, double lam[2]) {
+  const double hw2 = 0.5 * omega * omega;
+  if (d.N == 1) {  // single dof (n = 1, p = 2, Dirichlet): lambda = A/M exactly
+    const double m = s_bub_diag(0.0, 1.0, d.delta[0], 0);
+    const double a = s_bub_diag(1.0, hw2, d.delta[0], 0);
+    lam[0] = lam[1] = a / m;
+    return;
+  }
+  const double len = d.xs[d.n] - d.xs[0];
+  const double pi = 3.141592653589793238462643383279502884;
+  lam[0] = d.bc == 0 ? pi * pi / (len * len) + hw2 : hw2;
+  double h = d.delta[0];
+  for (double x : d.delta) h = std::min(h, x);
+  const double p2 = (double)d.p * d.p;
+  // Lemma 5.2: lambda_max(A, M) <= (24 p^4 + w^2 h^2) / (2 h^2)
+  double hi = std::max((24.0 * p2 * p2 + omega * omega * h * h) / (2.0 * h * h), 2.0 * lam[0]);
+  for (int it = 0; it < 200 && !spd_host(d, -1.0, hi - hw2); ++it) hi *= 2.0;
+  double lo = lam[0];
+  while (hi - lo > 1e-13 * hi) {
+    const double mid = lo + 0.5 * (hi - lo);
+    if (spd_host(d, -1.0, mid - hw2))
+      hi = mid;
+    else
+      lo = mid;
+  }
+  lam[1] = hi;
+}
+
+/* ---------------- Zolotarev shifts in binary128 (reading R5) ---------------- */
+typedef __float128 f128;
+
+f128 agm128(f128 a, f128 b) {
+  while (fabsq(a - b) > 1e-33Q * fabsq(a)) {
+    const f128 m = 0.5Q * (a + b);
+    b = sqrtq(a * b);
+    a = m;
+  }
+  return 0.5Q * (a + b);
+}
+
+/* Jacobi dn(u | k) for 0 <= u <= K/2 given k' (R5):
+ * k' >= 1e-8: descending Landen (arithmetic-geometric mean) scheme;
+ * k' <  1e-8: dn = sech u + (k'^2/4)(sinh u cosh u + u) tanh u sech u
+ *             (first order in k'^2 near k = 1; remainder O(k'^2) relative). */
+f128 dn_half(f128 u, f128 kp) {
+  if (kp >= 1.0Q) return 1.0Q;
+  if (kp < 1e-8Q) {
+    const f128 c = coshq(u), s = sinhq(u);
+    return 1.0Q / c + 0.25Q * kp * kp * (s * c + u) * (s / c) / c;
+  }
+  f128 A[80], Cc[80];
+  f128 a = 1.0Q, b = kp, c = sqrtq((1.0Q - kp) * (1.0Q + kp));
+  int N = 0;
+  while (fabsq(c) > 1e-34Q && N < 78) {
+    const f128 an = 0.5Q * (a + b);
+    c = 0.5Q * (a - b);
+    b = sqrtq(a * b);
+    a = an;
+    ++N;
+    A[N] = a;
+    Cc[N] = c;
+  }
+  f128 ph = ldexpq(a, N) * u, ph1 = ph;
+  for (int i = N; i >= 1; --i) {
+    ph1 = ph;
+    ph = 0.5Q * (ph + asinq(Cc[i] / A[i] * sinq(ph)));
+  }
+  return N == 0 ? 1.0Q : cosq(ph) / cosq(ph1 - ph);
+}
+
+f128 dn128(f128 u, f128 K, f128 kp) {
+  return (2 * u <= K) ? dn_half(u, kp) : kp / dn_half(K - u, kp);
+}
+
+int zolotarev(double a, double b, double c, double d, double tol, int& J, double& gamma, std::vector<double>& P,
+              std::vector<double>& Q) {
+  const f128 A = a, B = b, C = c, D = d;
+  const f128 g = fabsq(C - A) * fabsq(D - B) / (fabsq(C - B) * fabsq(D - A));
+  gamma = (double)g;
+  const f128 pi = M_PIq;
+  const f128 jr = logq(16.0Q * g) * logq(4.0Q / (f128)tol) / (pi * pi);
+  if (!(jr == jr) || jr > 1e6Q) return set_err(HPFEM_ENUMERIC, "non-finite or huge J");
+  J = (int)ceilq(jr);
+  if (J < 1) J = 1;
+  const f128 al = 2.0Q * g - 1.0Q + 2.0Q * sqrtq(g * g - g);  // cross-ratio image of gamma
+  const f128 kp = 1.0Q / al;
+  const f128 K = pi / (2.0Q * agm128(1.0Q, kp));
+  P.resize(J);
+  Q.resize(J);
+  const bool sym = (c == -b) && (d == -a);
+  // general Moebius T with T(-al)=a, T(-1)=b, T(1)=c as a 2x2 matrix:
+  // S_z sends (-al,-1,1) -> (0,1,inf), S_w sends (a,b,c) -> (0,1,inf), T = S_w^{-1} S_z
+  const f128 z1 = -al, z2 = -1.0Q, z3 = 1.0Q;
+  const f128 sz[4] = {z2 - z3, -z1 * (z2 - z3), z2 - z1, -z3 * (z2 - z1)};
+  const f128 sw[4] = {B - C, -A * (B - C), B - A, -C * (B - A)};
+  const f128 iw[4] = {sw[3], -sw[1], -sw[2], sw[0]};  // adjugate = inverse up to scale
+  const f128 T[4] = {iw[0] * sz[0] + iw[1] * sz[2], iw[0] * sz[1] + iw[1] * sz[3], iw[2] * sz[0] + iw[3] * sz[2],
+                     iw[2] * sz[1] + iw[3] * sz[3]};
+  auto mob = [&](f128 z) { return (T[0] * z + T[1]) / (T[2] * z + T[3]); };
+  for (int j = 1; j <= J; ++j) {
+    const f128 u = (f128)(2 * j - 1) * K / (2.0Q * J);
+    const f128 dn = dn128(u, K, kp);
+    if (sym) {
+      // T(z) = -b/z (al = b/a): p_j = a/dn_j, q_j = -p_j
+      P[j - 1] = (double)(A / dn);
+      Q[j - 1] = -P[j - 1];
+    } else {
+      P[j - 1] = (double)mob(-al * dn);
+      Q[j - 1] = (double)mob(al * dn);
+    }
+    if (!std::isfinite(P[j - 1]) || !std::isfinite(Q[j - 1]) || !(P[j - 1] > 0) || !(Q[j - 1] < 0))
+      return set_err(HPFEM_ENUMERIC, "non-finite or mis-signed shift");
+  }
+  return HPFEM_OK;
+}
+
+}  // namespace
+
+/* ======================================================================= */
+struct hpfem_plan_s {
+  DirHost hx, hy;
+  DirDev dx{}, dy{};
+  double omega = 0, tol = 0;
+  int J = 0;
+  double lam_x[2] = {0, 0}, lam_y[2] = {0, 0}, gamma = 0;
+  std::vector<double> P, Q;
+  size_t sx = 0, sy = 0;          // factor strides
+  double* fx = nullptr;           // J sets (x-solves)
+  double* fy = nullptr;           // J+1 sets (y-solves, last = mass)
+  double* d_delta = nullptr;      // [n_x | n_y]
+  double* d_shift = nullptr;      // kap/sig arrays
+  int* d_err = nullptr;
+  double* work = nullptr;         // N_x x N_y
+  long long launches = 0;
+  // profiling (hpfem_plan_profile)
+  std::vector<cudaEvent_t> ev;
+  int ev_used = 0;
+  struct Rec { int kind, e0, e1; double bytes; };
+  std::vector<Rec> recs;
+};
+
+namespace {
+
+int count_launch(hpfem_plan_t pl, cudaError_t e, const char* where) {
+  if (e != cudaSuccess) return cuda_err(e, where);
+  ++pl->launches;
+  return HPFEM_OK;
+}
+
+void free_events(hpfem_plan_t pl) {
+  for (cudaEvent_t e : pl->ev) cudaEventDestroy(e);
+  pl->ev.clear();
+  pl->ev_used = 0;
+  pl->recs.clear();
+}
+
+/* record an event if profiling is on; returns its index or -1 */
+int prof_mark(hpfem_plan_t pl, cudaStream_t st) {
+  if (pl->ev_used >= (int)pl->ev.size()) return -1;
+  if (cudaEventRecord(pl->ev[pl->ev_used], st) != cudaSuccess) return -1;
+  return pl->ev_used++;
+}
+
+void prof_add(hpfem_plan_t pl, int kind, int e0, int e1, double bytes) {
+  if (e0 >= 0 && e1 >= 0) pl->recs.push_back({kind, e0, e1, bytes});
+}
+
+void free_plan(hpfem_plan_t pl) {
+  if (!pl) return;
+  free_events(pl);
+  cudaFree(pl->fx);
+  cudaFree(pl->fy);
+  cudaFree(pl->d_delta);
+  cudaFree(pl->d_shift);
+  cudaFree(pl->d_err);
+  cudaFree(pl->work);
+  delete pl;
+}
+
+int validate_mesh(const double* xs, int n, int p) {
+  if (!xs) return set_err(HPFEM_EINVAL, "null breakpoints");
+  if (n < 1) return set_err(HPFEM_EINVAL, "n < 1");
+  if (p < 2) return set_err(HPFEM_EINVAL, "p < 2");
+  for (int e = 0; e < n; ++e)
+    if (!(xs[e + 1] > xs[e]) || !std::isfinite(xs[e + 1]) || !std::isfinite(xs[e]))
+      return set_err(HPFEM_EINVAL, "breakpoints must be finite and strictly increasing");
+  return HPFEM_OK;
+}
+
+int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int py, double omega, int bc, double tol,
+               cudaStream_t st, hpfem_plan_t* out) {
+  if (!out) return set_err(HPFEM_EINVAL, "null out");
+  *out = nullptr;
+  int rc;
+  if ((rc = validate_mesh(xs, nx, px)) != HPFEM_OK) return rc;
+  if ((rc = validate_mesh(ys, ny, py)) != HPFEM_OK) return rc;
+  if (bc != HPFEM_BC_DIRICHLET && bc != HPFEM_BC_NEUMANN) return set_err(HPFEM_EINVAL, "bad bc");
+  if (!(tol > 0.0 && tol < 1.0)) return set_err(HPFEM_EINVAL, "tol must lie in (0,1)");
+  if (!std::isfinite(omega)) return set_err(HPFEM_EINVAL, "omega not finite");
+  if (bc == HPFEM_BC_NEUMANN && omega == 0.0)
+    return set_err(HPFEM_EINVAL, "Neumann requires omega != 0 (P:L812)");
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0) return set_err(HPFEM_ECUDA, "no CUDA device (no CPU fallback)");
+
+  hpfem_plan_t pl = new hpfem_plan_s();
+  pl->hx = make_dir(xs, nx, px, bc);
+  pl->hy = make_dir(ys, ny, py, bc);
+  pl->omega = omega;
+  pl->tol = tol;
+  spectral_interval(pl->hx, omega, pl->lam_x);
+  spectral_interval(pl->hy, omega, pl->lam_y);
+  for (double v : {pl->lam_x[0], pl->lam_x[1], pl->lam_y[0], pl->lam_y[1]})
+    if (!std::isfinite(v) || !(v > 0)) {
+      free_plan(pl);
+      return set_err(HPFEM_ENUMERIC, "non-finite spectral bound");
+    }
+  // [a,b] = sigma(A_x, M_x); [c,d] = sigma(B, C) = -sigma(A_y, M_y)  (eq. adi:poisson)
+  if ((rc = zolotarev(pl->lam_x[0], pl->lam_x[1], -pl->lam_y[1], -pl->lam_y[0], tol, pl->J, pl->gamma, pl->P,
+                      pl->Q)) != HPFEM_OK) {
+    free_plan(pl);
+    return rc;
+  }
+  const int J = pl->J;
+  const double hw2 = 0.5 * omega * omega;
+  // device allocations
+  auto fail_cuda = [&](cudaError_t e, const char* w) {
+    free_plan(pl);
+    return e == cudaErrorMemoryAllocation ? set_err(HPFEM_ENOMEM, std::string(w) + ": out of device memory")
+                                          : cuda_err(e, w);
+  };
+  DirHost& hx = pl->hx;
+  DirHost& hy = pl->hy;
+  if ((ce = cudaMalloc(&pl->d_delta, sizeof(double) * (nx + ny))) != cudaSuccess) return fail_cuda(ce, "alloc");
+  if ((ce = cudaMemcpyAsync(pl->d_delta, hx.delta.data(), sizeof(double) * nx, cudaMemcpyHostToDevice, st)) !=
+      cudaSuccess)
+    return fail_cuda(ce, "copy");
+  if ((ce = cudaMemcpyAsync(pl->d_delta + nx, hy.delta.data(), sizeof(double) * ny, cudaMemcpyHostToDevice, st)) !=
+      cudaSuccess)
+    return fail_cuda(ce, "copy");
+  auto mkdev = [](const DirHost& h, const double* dd) {
+    DirDev d;
+    d.n = h.n; d.p = h.p; d.bc = h.bc; d.nh = h.nh; d.N = h.N; d.nb = h.nb; d.delta = dd;
+    return d;
+  };
+  pl->dx = mkdev(hx, pl->d_delta);
+  pl->dy = mkdev(hy, pl->d_delta + nx);
+  pl->sx = fac_stride(pl->dx);
+  pl->sy = fac_stride(pl->dy);
+  // shift parameter tables: x: J sets (kap=1, sig = w^2/2 - q_j); y: J sets (sig = w^2/2 + p_j) + mass
+  std::vector<double> sh(4 * (size_t)(J + 1), 0.0);
+  double* kx = sh.data();
+  double* sgx = kx + (J + 1);
+  double* ky = sgx + (J + 1);
+  double* sgy = ky + (J + 1);
+  for (int j = 0; j < J; ++j) {
+    kx[j] = 1.0;
+    sgx[j] = hw2 - pl->Q[j];
+    ky[j] = 1.0;
+    sgy[j] = hw2 + pl->P[j];
+  }
+  ky[J] = 0.0;
+  sgy[J] = 1.0;  // C = M_y for the final W_J C^{-1}
+  if ((ce = cudaMalloc(&pl->d_shift, sizeof(double) * sh.size())) != cudaSuccess) return fail_cuda(ce, "alloc");
+  if ((ce = cudaMemcpyAsync(pl->d_shift, sh.data(), sizeof(double) * sh.size(), cudaMemcpyHostToDevice, st)) !=
+      cudaSuccess)
+    return fail_cuda(ce, "copy");
+  if ((ce = cudaMalloc(&pl->fx, sizeof(double) * pl->sx * J)) != cudaSuccess) return fail_cuda(ce, "alloc fx");
+  if ((ce = cudaMalloc(&pl->fy, sizeof(double) * pl->sy * (J + 1))) != cudaSuccess) return fail_cuda(ce, "alloc fy");
+  if ((ce = cudaMalloc(&pl->d_err, sizeof(int) * 8)) != cudaSuccess) return fail_cuda(ce, "alloc");
+  if ((ce = cudaMemsetAsync(pl->d_err, 0, sizeof(int) * 8, st)) != cudaSuccess) return fail_cuda(ce, "memset");
+  if ((ce = cudaMemsetAsync(pl->fx, 0, sizeof(double) * pl->sx * J, st)) != cudaSuccess) return fail_cuda(ce, "memset");
+  if ((ce = cudaMemsetAsync(pl->fy, 0, sizeof(double) * pl->sy * (J + 1), st)) != cudaSuccess)
+    return fail_cuda(ce, "memset");
+  if ((ce = cudaMalloc(&pl->work, sizeof(double) * (size_t)hx.N * hy.N)) != cudaSuccess)
+    return fail_cuda(ce, "alloc workspace");
+  const double* dsh = pl->d_shift;
+  if ((ce = launch_factor(pl->dx, dsh, dsh + (J + 1), J, pl->fx, pl->sx, pl->d_err, st)) != cudaSuccess)
+    return fail_cuda(ce, "factor x");
+  if ((ce = launch_factor(pl->dy, dsh + 2 * (J + 1), dsh + 3 * (J + 1), J + 1, pl->fy, pl->sy, pl->d_err + 4, st)) !=
+      cudaSuccess)
+    return fail_cuda(ce, "factor y");
+  int herr[8];
+  if ((ce = cudaMemcpyAsync(herr, pl->d_err, sizeof(herr), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return fail_cuda(ce, "copy err");
+  if ((ce = cudaStreamSynchronize(st)) != cudaSuccess) return fail_cuda(ce, "plan sync");
+  for (int dd = 0; dd < 2; ++dd)
+    if (herr[4 * dd]) {
+      char buf[256];
+      std::snprintf(buf, sizeof buf, "non-positive pivot: direction %c, shift set %d, %s %d, degree %d",
+                    dd ? 'y' : 'x', herr[4 * dd + 1], herr[4 * dd] == 1 ? "element" : "hat", herr[4 * dd + 2],
+                    herr[4 * dd + 3]);
+      free_plan(pl);
+      return set_err(HPFEM_ENOTPD, buf);
+    }
+  pl->launches = 4;
+  *out = pl;
+  return HPFEM_OK;
+}
+
+FacView fview(hpfem_plan_t pl, int dir, int set) {
+  const int J = pl->J;
+  const double hw2 = 0.5 * pl->omega * pl->omega;
+  if (dir == 0) return fac_view(pl->dx, pl->fx + pl->sx * set, 1.0, hw2 - pl->Q[set]);
+  if (set == J) return fac_view(pl->dy, pl->fy + pl->sy * set, 0.0, 1.0);
+  return fac_view(pl->dy, pl->fy + pl->sy * set, 1.0, hw2 + pl->P[set]);
+}
+
+bool overlap(const void* a, const void* b, size_t bytes) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + bytes && y < x + bytes;
+}
+
+/* One line-solve pass (bubble kernel + hat kernel).  Algorithmic bytes:
+ * per dof read G (if used), read the previous iterate (if any), write the
+ * output. */
+int run_step(hpfem_plan_t pl, const StepParams& P, cudaStream_t st, bool final_step) {
+  const double per = 8.0 * ((P.alphaG != 0.0 ? 1 : 0) + (P.mode != ST_NONE ? 1 : 0) + 1);
+  const int k0 = final_step ? 2 : 0, k1 = final_step ? 2 : 1;
+  const int e0 = prof_mark(pl, st);
+  int rc = count_launch(pl, launch_step_bubbles(P, st), "bubble kernel");
+  if (rc) return rc;
+  const int e1 = prof_mark(pl, st);
+  prof_add(pl, k0, e0, e1, per * (double)P.o.N * P.s.nb);
+  if (P.s.nh > 0) {
+    rc = count_launch(pl, launch_step_hats(P, st), "hat kernel");
+    if (rc) return rc;
+    const int e2 = prof_mark(pl, st);
+    prof_add(pl, k1, e1, e2, per * (double)P.o.N * P.s.nh);
+  }
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hpfem_last_error(void) { return t_err.c_str(); }
+
+int hpfem_plan_mesh(const double* xs, int n_x, int p_x, const double* ys, int n_y, int p_y, double omega, int bc,
+                    double tol, void* cuda_stream, hpfem_plan_t* out) {
+  t_err.clear();
+  return build_plan(xs, n_x, p_x, ys, n_y, p_y, omega, bc, tol, (cudaStream_t)cuda_stream, out);
+}
+
+int hpfem_plan(int n_x, int p_x, int n_y, int p_y, double a, double b, double c, double d, double omega, int bc,
+               double tol, void* cuda_stream, hpfem_plan_t* out) {
+  t_err.clear();
+  if (n_x < 1 || n_y < 1) return set_err(HPFEM_EINVAL, "n < 1");
+  if (!(b > a) || !(d > c)) return set_err(HPFEM_EINVAL, "empty domain");
+  std::vector<double> xs(n_x + 1), ys(n_y + 1);
+  for (int e = 0; e <= n_x; ++e) xs[e] = a + (b - a) * ((double)e / n_x);
+  for (int e = 0; e <= n_y; ++e) ys[e] = c + (d - c) * ((double)e / n_y);
+  return build_plan(xs.data(), n_x, p_x, ys.data(), n_y, p_y, omega, bc, tol, (cudaStream_t)cuda_stream, out);
+}
+
+int hpfem_plan_info(hpfem_plan_t pl, int* N_x, int* N_y, int* J, double* lam_x, double* lam_y, double* gamma) {
+  if (!pl) return set_err(HPFEM_EINVAL, "null plan");
+  if (N_x) *N_x = pl->hx.N;
+  if (N_y) *N_y = pl->hy.N;
+  if (J) *J = pl->J;
+  if (lam_x) { lam_x[0] = pl->lam_x[0]; lam_x[1] = pl->lam_x[1]; }
+  if (lam_y) { lam_y[0] = pl->lam_y[0]; lam_y[1] = pl->lam_y[1]; }
+  if (gamma) *gamma = pl->gamma;
+  return HPFEM_OK;
+}
+
+int hpfem_plan_shifts(hpfem_plan_t pl, double* p, double* q) {
+  if (!pl) return set_err(HPFEM_EINVAL, "null plan");
+  if (p) std::memcpy(p, pl->P.data(), sizeof(double) * pl->J);
+  if (q) std::memcpy(q, pl->Q.data(), sizeof(double) * pl->J);
+  return HPFEM_OK;
+}
+
+int hpfem_plan_launches(hpfem_plan_t pl, long long* launches) {
+  if (!pl || !launches) return set_err(HPFEM_EINVAL, "null argument");
+  *launches = pl->launches;
+  return HPFEM_OK;
+}
+
+int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !F || !U) return set_err(HPFEM_EINVAL, "null argument");
+  if (iters < 0 || iters > pl->J) return set_err(HPFEM_EINVAL, "iters must lie in [0, J]");
+  const size_t bytes = sizeof(double) * (size_t)pl->hx.N * pl->hy.N;
+  if (overlap(F, U, bytes)) return set_err(HPFEM_EINVAL, "F and U overlap");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  pl->launches = 0;
+  const double hw2 = 0.5 * pl->omega * pl->omega;
+  double* X1 = U;          // W_{j-1/2} (deferred along y), then U
+  double* X2 = pl->work;   // W_j      (deferred along x)
+  int rc;
+  for (int j = 0; j < iters; ++j) {
+    // half-step A: W_{j-1/2} = (G - (A_x - p_j M_x) W_{j-1}) (A_y + p_j M_y)^{-1}
+    StepParams A{};
+    A.dir = 1;
+    A.ld = pl->hy.N;
+    A.s = pl->dy;
+    A.o = pl->dx;
+    A.G = F;
+    A.alphaG = 1.0;
+    A.f = fview(pl, 1, j);
+    A.out = X1;
+    if (j == 0) {
+      A.mode = ST_NONE;  // W_0 = 0
+    } else {
+      const FacView prev = fview(pl, 0, j - 1);
+      A.mode = ST_APPLY;
+      A.Xp = X2;
+      A.kap_a = 1.0;
+      A.tau = hw2 - pl->P[j];
+      A.cvL = prev.vL;
+      A.cvR = prev.vR;
+    }
+    if ((rc = run_step(pl, A, st, false))) return rc;
+    // half-step B: W_j = (A_x - q_j M_x)^{-1} (G - W_{j-1/2} (A_y + q_j M_y))
+    StepParams B{};
+    B.dir = 0;
+    B.ld = pl->hy.N;
+    B.s = pl->dx;
+    B.o = pl->dy;
+    B.G = F;
+    B.alphaG = 1.0;
+    B.f = fview(pl, 0, j);
+    B.out = X2;
+    B.mode = ST_APPLY;
+    B.Xp = X1;
+    B.kap_a = 1.0;
+    B.tau = hw2 + pl->Q[j];
+    B.cvL = A.f.vL;
+    B.cvR = A.f.vR;
+    if ((rc = run_step(pl, B, st, false))) return rc;
+  }
+  if (iters == 0) {
+    cudaError_t ce = cudaMemsetAsync(U, 0, bytes, st);
+    return ce == cudaSuccess ? HPFEM_OK : cuda_err(ce, "memset");
+  }
+  // RETURN W_J C^{-1}: y-solves with the mass factor, then materialise
+  StepParams Fin{};
+  Fin.dir = 1;
+  Fin.ld = pl->hy.N;
+  Fin.s = pl->dy;
+  Fin.o = pl->dx;
+  Fin.G = nullptr;
+  Fin.alphaG = 0.0;
+  Fin.f = fview(pl, 1, pl->J);
+  Fin.out = X1;
+  Fin.mode = ST_CORR;
+  Fin.Xp = X2;
+  const FacView last = fview(pl, 0, iters - 1);
+  Fin.cvL = last.vL;
+  Fin.cvR = last.vR;
+  if ((rc = run_step(pl, Fin, st, true))) return rc;
+  const int e0 = prof_mark(pl, st);
+  rc = count_launch(pl, launch_correct_rows(pl->dy, pl->hx.N, Fin.f.vL, Fin.f.vR, U, st), "correct kernel");
+  prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);  // not algorithmic: the deferred correction pass
+  return rc;
+}
+
+int hpfem_solve(hpfem_plan_t pl, const double* F, double* U, void* cuda_stream) {
+  if (!pl) return set_err(HPFEM_EINVAL, "null plan");
+  return hpfem_solve_iters(pl, F, U, pl->J, cuda_stream);
+}
+
+int hpfem_apply(hpfem_plan_t pl, const double* U, double* F, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !U || !F) return set_err(HPFEM_EINVAL, "null argument");
+  if (overlap(U, F, sizeof(double) * (size_t)pl->hx.N * pl->hy.N)) return set_err(HPFEM_EINVAL, "U and F overlap");
+  pl->launches = 0;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int e0 = prof_mark(pl, st);
+  const int rc = count_launch(pl, launch_apply2d(pl->dx, pl->dy, pl->omega, U, F, st), "apply");
+  prof_add(pl, 4, e0, prof_mark(pl, st), 16.0 * pl->hx.N * pl->hy.N);
+  return rc;
+}
+
+int hpfem_load(hpfem_plan_t pl, const double* F_leg, double* G, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !F_leg || !G) return set_err(HPFEM_EINVAL, "null argument");
+  const size_t bl = sizeof(double) * (size_t)(pl->hx.p + 1) * pl->hx.n * (pl->hy.p + 1) * pl->hy.n;
+  const size_t bg = sizeof(double) * (size_t)pl->hx.N * pl->hy.N;
+  const char* a = (const char*)F_leg;
+  const char* b = (const char*)G;
+  if (a < b + bg && b < a + bl) return set_err(HPFEM_EINVAL, "F_leg and G overlap");
+  pl->launches = 0;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int e0 = prof_mark(pl, st);
+  const int rc = count_launch(pl, launch_load2d(pl->dx, pl->dy, F_leg, G, st), "load");
+  prof_add(pl, 3, e0, prof_mark(pl, st), (double)bl + (double)bg);
+  return rc;
+}
+
+int hpfem_plan_profile(hpfem_plan_t pl, int capacity) {
+  if (!pl || capacity < 0) return set_err(HPFEM_EINVAL, "bad argument");
+  free_events(pl);
+  pl->ev.resize(capacity);
+  for (int i = 0; i < capacity; ++i) {
+    cudaError_t ce = cudaEventCreate(&pl->ev[i]);
+    if (ce != cudaSuccess) {
+      pl->ev.resize(i);
+      free_events(pl);
+      return cuda_err(ce, "event create");
+    }
+  }
+  return HPFEM_OK;
+}
+
+int hpfem_plan_profile_read(hpfem_plan_t pl, double* ms, long long* n, double* bytes) {
+  if (!pl || !ms || !n || !bytes) return set_err(HPFEM_EINVAL, "null argument");
+  for (int k = 0; k < 5; ++k) {
+    ms[k] = 0.0;
+    n[k] = 0;
+    bytes[k] = 0.0;
+  }
+  if (pl->ev_used > 0) {
+    cudaError_t ce = cudaEventSynchronize(pl->ev[pl->ev_used - 1]);
+    if (ce != cudaSuccess) return cuda_err(ce, "event sync");
+  }
+  for (const auto& r : pl->recs) {
+    float t = 0.f;
+    cudaError_t ce = cudaEventElapsedTime(&t, pl->ev[r.e0], pl->ev[r.e1]);
+    if (ce != cudaSuccess) return cuda_err(ce, "event elapsed");
+    ms[r.kind] += t;
+    n[r.kind] += 1;
+    bytes[r.kind] += r.bytes;
+  }
+  pl->recs.clear();
+  pl->ev_used = 0;
+  return HPFEM_OK;
+}
+
+void hpfem_plan_destroy(hpfem_plan_t pl) { free_plan(pl); }
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+"""CPU-side checks of the C ABI library (no compute calls without a GPU):
+it builds, loads, exports every symbol include/hpfem.h declares, shares no
+code with the oracle, and refuses to run without a device (no fallback)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "hpfem.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hpfem_[a-z_]+)\s*\(", src)))
+
+
+def _lib_path():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("_b", os.path.join(ROOT, "paper_2402_11299_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build()
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib_path()
+    names = _declared()
+    assert len(names) >= 12
+    L = ctypes.CDLL(lib)
+    for n in names:
+        assert hasattr(L, n), n
+    nm = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True).stdout
+    assert "oracle_" not in nm
+
+
+def test_binding_names_match_header():
+    import paper_2402_11299_b200 as hp
+
+    for n in _declared():
+        assert n in hp.EXPORTS and callable(getattr(hp, n)), n
+
+
+def test_no_shared_code_with_oracle():
+    """The product sources never include / import the oracle, and vice versa."""
+    prod = os.path.join(ROOT, "paper_2402_11299_b200")
+    for dp, _, fs in os.walk(prod):
+        for f in fs:
+            if f.endswith((".py", ".cpp", ".cu", ".h")):
+                s = open(os.path.join(dp, f)).read()
+                for bad in ("import oracle", "from oracle", "hpfem_oracle", "liboracle"):
+                    assert bad not in s, (f, bad)
+    for f in ("hpfem_oracle.cpp", "__init__.py"):
+        s = open(os.path.join(ROOT, "oracle", f)).read()
+        for bad in ("ops1d.h", "hpfem_internal", "import paper_2402_11299_b200", "from paper_2402_11299_b200",
+                    "libhpfem_b200"):
+            assert bad not in s, (f, bad)
+
+
+def test_refuses_without_device():
+    """No GPU here: hpfem_plan must fail with HPFEM_ECUDA, never compute on
+    the CPU."""
+    import torch
+
+    if torch.cuda.is_available():
+        return
+    L = ctypes.CDLL(_lib_path())
+    L.hpfem_plan_mesh.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_int,
+                                  ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                  ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+    xs = np.linspace(0, 1, 3)
+    h = ctypes.c_void_p()
+    p = xs.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    rc = L.hpfem_plan_mesh(p, 2, 4, p, 2, 4, 0.0, 0, 1e-10, None, ctypes.byref(h))
+    assert rc == -3  # HPFEM_ECUDA
+    rc = L.hpfem_plan_mesh(p, 2, 1, p, 2, 4, 0.0, 0, 1e-10, None, ctypes.byref(h))
+    assert rc == -1  # HPFEM_EINVAL is checked before touching the device

@@ -1,0 +1,191 @@
+"""GPU (CUDA, sm_100a) vs oracle parity, through the C ABI binding.
+
+Tolerance (north_star): relative difference <= 1e-10 in
+the L2(Omega) norm of the FEM solution -- the norm of Lemma 5.1,
+reading R12 -- with the same J (exact) and shifts (to <= 1e-11, the
+independent lambda_max bisections agree to that level).  The plain
+coefficient 2-norm difference is printed for information.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_util import gpu_apply, gpu_load, gpu_plan, gpu_solve, parity, torch_cuda
+
+pytestmark = pytest.mark.gpu
+
+RNG = np.random.default_rng(7)
+L2_TOL = 1e-10
+
+
+def rmesh(n, a=0.0, b=1.0, seed=0):
+    w = np.random.default_rng(seed).uniform(0.3, 1.7, size=n)
+    xs = np.concatenate([[0.0], np.cumsum(w)])
+    return a + (b - a) * xs / xs[-1]
+
+
+SMALL = [
+    # (xs, px, ys, py, omega, bc, tol)
+    (np.array([-1.0, 1.0]), 2, np.array([-1.0, 1.0]), 2, 0.0, 0, 1e-10),  # N = 1
+    (np.array([0.0, 1.0]), 6, np.array([0.0, 1.0]), 5, 1.0, 0, 1e-12),  # single element: no hats
+    (np.linspace(0, 1, 3), 2, np.linspace(0, 1, 4), 2, 0.0, 0, 1e-12),  # p = 2: empty odd chains
+    (np.linspace(0, 1, 4), 3, np.linspace(0, 2, 3), 7, 3.0, 0, 1e-12),
+    (rmesh(5, 0, 1, 1), 9, rmesh(4, 0, 3, 2), 4, 1.0, 1, 1e-12),
+    (np.array([0.0, 1.0]), 4, np.array([0.0, 2.0]), 3, 2.0, 1, 1e-12),  # Neumann n = 1: 2 hats
+    (W.graded_mesh(0, 1, 8, 0.6), 6, W.graded_mesh(0, 1, 8, 0.6), 6, 1.0, 1, 1e-10),
+    (np.linspace(-1, 1, 6), 12, np.linspace(-1, 1, 7), 10, 10.0, 0, 1e-10),
+    (rmesh(3, 0, 1, 3), 40, rmesh(2, 0, 1, 4), 70, 0.0, 0, 1e-12),  # chains > 32
+    (np.linspace(0, 1, 3), 150, np.linspace(0, 1, 2), 140, 0.5, 0, 1e-8),  # chains > 64 (long path)
+]
+
+
+@pytest.mark.parametrize("case", range(len(SMALL)))
+def test_small_cases(case):
+    xs, px, ys, py, om, bc, tol = SMALL[case]
+    plan = gpu_plan(xs, px, ys, py, om, bc, tol)
+    ref = oracle.plan(xs, px, ys, py, om, bc, tol)
+    assert plan.J == ref["J"]
+    p, q = plan.shifts()
+    np.testing.assert_allclose(p, ref["p"], rtol=1e-11)
+    np.testing.assert_allclose(q, ref["q"], rtol=1e-11)
+    G = RNG.standard_normal((plan.Nx, plan.Ny))
+    U = gpu_solve(plan, G)
+    Uref, J = oracle.adi_solve(xs, px, ys, py, om, bc, tol, G)
+    l2, plain = parity(xs, px, ys, py, bc, U, Uref)
+    print(f"case {case}: N={plan.Nx}x{plan.Ny} J={J} L2 {l2:.2e} plain {plain:.2e}")
+    assert l2 <= L2_TOL
+
+
+@pytest.mark.parametrize("case", [3, 4, 5, 7])
+def test_lemma51_against_dense(case):
+    """The GPU solution itself meets Lemma 5.1 against the dense
+    Kronecker solution of eq. adi:poisson."""
+    xs, px, ys, py, om, bc, tol = SMALL[case]
+    plan = gpu_plan(xs, px, ys, py, om, bc, tol)
+    Kx, Mx = oracle.operator_dense(xs, px, bc, 1, 0), oracle.operator_dense(xs, px, bc, 0, 1)
+    Ky, My = oracle.operator_dense(ys, py, bc, 1, 0), oracle.operator_dense(ys, py, bc, 0, 1)
+    Ax, Ay = Kx + om * om / 2 * Mx, Ky + om * om / 2 * My
+    G = RNG.standard_normal((plan.Nx, plan.Ny))
+    Us = np.linalg.solve(np.kron(Ax, My) + np.kron(Mx, Ay), G.reshape(-1)).reshape(G.shape)
+    U = gpu_solve(plan, G)
+    V, L = np.linalg.cholesky(Mx).T, np.linalg.cholesky(My).T
+    err = np.linalg.norm(V @ (U - Us) @ L.T, 2) / np.linalg.norm(V @ Us @ L.T, 2)
+    floor = 1e-13 * np.linalg.cond(Mx) * np.linalg.cond(My)
+    assert err <= tol + floor
+
+
+def _config_inputs(i):
+    c = W.CONFIGS[i]
+    xs, ys = c.breakpoints()
+    Fleg = W.f_leg(c, seed=0)
+    return c, xs, ys, Fleg
+
+
+@pytest.mark.parametrize("i", [1, 2, 3, 4, 5])
+def test_config_plan(i):
+    """J exact and shifts / intervals to 1e-11 on every configuration."""
+    c = W.CONFIGS[i]
+    xs, ys = c.breakpoints()
+    plan = gpu_plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
+    ref = oracle.plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
+    assert (plan.Nx, plan.Ny, plan.J) == (ref["Nx"], ref["Ny"], ref["J"])
+    np.testing.assert_allclose(plan.lam_x, ref["lam_x"], rtol=1e-11)
+    np.testing.assert_allclose(plan.lam_y, ref["lam_y"], rtol=1e-11)
+    p, q = plan.shifts()
+    np.testing.assert_allclose(p, ref["p"], rtol=1e-11)
+    np.testing.assert_allclose(q, ref["q"], rtol=1e-11)
+
+
+@pytest.mark.parametrize("i", [1, 2, 3])
+def test_config_load(i):
+    """hpfem_load (K8) vs oracle_load at full size."""
+    c, xs, ys, Fleg = _config_inputs(i)
+    plan = gpu_plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
+    G = gpu_load(plan, Fleg)
+    Gref = oracle.load(xs, c.px, ys, c.py, c.bc, Fleg)
+    assert np.abs(G - Gref).max() <= 1e-14 * np.abs(Gref).max()
+
+
+@pytest.mark.parametrize("i", [1, 2, 3])
+def test_config_apply(i):
+    """hpfem_apply (K7) vs oracle_apply at full size."""
+    c = W.CONFIGS[i]
+    xs, ys = c.breakpoints()
+    plan = gpu_plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
+    U = W.random_field((plan.Nx, plan.Ny), 11)
+    F = gpu_apply(plan, U)
+    Fref = oracle.apply(xs, c.px, ys, c.py, c.omega, c.bc, U)
+    assert np.abs(F - Fref).max() <= 1e-12 * np.abs(Fref).max()
+
+
+@pytest.mark.parametrize("i", [1, 2, 3, 4])
+def test_config_full_solve(i):
+    """Full ADI solve (all J iterations) vs the oracle at full size."""
+    c, xs, ys, Fleg = _config_inputs(i)
+    plan = gpu_plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
+    G = oracle.load(xs, c.px, ys, c.py, c.bc, Fleg)
+    U = gpu_solve(plan, G)
+    Uref, J = oracle.adi_solve(xs, c.px, ys, c.py, c.omega, c.bc, c.tol, G)
+    assert J == plan.J
+    l2, plain = parity(xs, c.px, ys, c.py, c.bc, U, Uref)
+    print(f"config {i}: J={J} L2 {l2:.3e} plain {plain:.3e}")
+    assert l2 <= L2_TOL
+
+
+@pytest.mark.parametrize("iters", [1, 2])
+def test_config5_truncated(iters):
+    """Config 5 at full size (16385^2, graded Neumann): the first `iters`
+    ADI iterations + W C^{-1}, GPU vs oracle (the full 162-iteration oracle
+    solve takes ~20 CPU-minutes; see DESIGN.md "Parity" for config 5)."""
+    c, xs, ys, Fleg = _config_inputs(5)
+    plan = gpu_plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
+    G = oracle.load(xs, c.px, ys, c.py, c.bc, Fleg)
+    U = gpu_solve(plan, G, iters=iters)
+    Uref, _ = oracle.adi_solve(xs, c.px, ys, c.py, c.omega, c.bc, c.tol, G, iters=iters)
+    l2, plain = parity(xs, c.px, ys, c.py, c.bc, U, Uref)
+    print(f"config 5, {iters} iterations: L2 {l2:.3e} plain {plain:.3e}")
+    assert l2 <= L2_TOL
+
+
+def test_iters_zero_and_zero_rhs():
+    xs, px, ys, py, om, bc, tol = SMALL[4]
+    plan = gpu_plan(xs, px, ys, py, om, bc, tol)
+    G = RNG.standard_normal((plan.Nx, plan.Ny))
+    assert np.all(gpu_solve(plan, G, iters=0) == 0)
+    assert np.all(gpu_solve(plan, np.zeros_like(G)) == 0)
+
+
+def test_errors():
+    import paper_2402_11299_b200 as hp
+
+    torch = torch_cuda()
+    xs = np.linspace(0, 1, 3)
+    with pytest.raises(hp.HpfemError) as e:
+        hp.Plan(xs, 4, xs, 4, 0.0, 1, 1e-10)  # Neumann needs omega != 0
+    assert e.value.code == hp.HPFEM_EINVAL
+    with pytest.raises(hp.HpfemError):
+        hp.Plan(xs, 1, xs, 4, 0.0, 0, 1e-10)  # p < 2
+    with pytest.raises(hp.HpfemError):
+        hp.Plan(np.array([0.0, 0.5, 0.5]), 4, xs, 4, 0.0, 0, 1e-10)  # not increasing
+    with pytest.raises(hp.HpfemError):
+        hp.Plan(xs, 4, xs, 4, 0.0, 0, 1.5)  # tol
+    plan = hp.Plan(xs, 4, xs, 4, 0.0, 0, 1e-10)
+    A = torch.zeros((plan.Nx, plan.Ny), dtype=torch.float64, device="cuda")
+    with pytest.raises(hp.HpfemError) as e:
+        plan.solve(A, A)
+    assert e.value.code == hp.HPFEM_EINVAL
+    with pytest.raises(hp.HpfemError):
+        plan.solve(A, torch.empty_like(A), iters=plan.J + 1)
+
+
+def test_solve_plan_reuse_and_linearity():
+    xs, px, ys, py, om, bc, tol = SMALL[3]
+    plan = gpu_plan(xs, px, ys, py, om, bc, tol)
+    G1, G2 = RNG.standard_normal((2, plan.Nx, plan.Ny))
+    U1, U2 = gpu_solve(plan, G1), gpu_solve(plan, G2)
+    U3 = gpu_solve(plan, 2 * G1 - 3 * G2)
+    assert np.abs(U3 - (2 * U1 - 3 * U2)).max() <= 1e-11 * np.abs(U3).max()
+    assert np.array_equal(gpu_solve(plan, G1), U1)  # deterministic
