@@ -54,6 +54,7 @@ _i = ctypes.c_int
 def _declare(L):
     L.oracle_last_error.restype = ctypes.c_char_p
     L.oracle_dim.argtypes = [_i, _i, _i]
+    L.oracle_threads.restype = _i
     L.oracle_operator_dense.argtypes = [_dp, _i, _i, _i, _d, _d, _dp]
     L.oracle_operator_coo.argtypes = [_dp, _i, _i, _i, _i, _ip, _ip, _dp, _ip]
     L.oracle_factor_dense.argtypes = [_dp, _i, _i, _i, _d, _d, _dp, _ip]
@@ -86,6 +87,11 @@ def _ptr(a):
 
 def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def threads():
+    """OpenMP threads used by the oracle's line loops."""
+    return lib().oracle_threads()
 
 
 def dim(n, p, bc):

@@ -33,6 +33,7 @@
  * OpenMP is used only across independent lines (rows / columns) of the
  * 2D arrays; it does not change any arithmetic.
  */
+#include <omp.h>
 #include <quadmath.h>
 
 #include <cmath>
@@ -609,6 +610,9 @@ int make_problem(const double* xs, int nx, int px, const double* ys, int ny, int
 extern "C" {
 
 const char* oracle_last_error(void) { return g_err.c_str(); }
+
+/* OpenMP threads the oracle's line loops use (bench.py cpu_baseline.cores) */
+int oracle_threads(void) { return omp_get_max_threads(); }
 
 /* N of the 1D space */
 int oracle_dim(int n, int p, int bc) { return (bc == 0 ? n - 1 : n + 1) + (p - 1) * n; }

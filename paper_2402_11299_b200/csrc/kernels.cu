@@ -22,6 +22,7 @@
  *   K7  k_apply2d: F = A_x U M_y + M_x U A_y.     K8 k_load2d: G = R^T M_P F M_P R.
  */
 #include <cstdint>
+#include <cstdlib>
 
 #include "hpfem_internal.h"
 #include "ops1d.h"
@@ -248,15 +249,26 @@ __device__ __forceinline__ size_t addr(int l, int d, int ld) {
   return DIR == 0 ? (size_t)d * ld + l : (size_t)l * ld + d;
 }
 
-/* r(l, d) = alphaG G(l,d) + sum_q w_q Xp(idx_q, d) */
+/* r(l, d) = alphaG G(l,d) + sum_q w_q Xp(idx_q, d)   (read-only inputs) */
 template <int DIR>
-__device__ __forceinline__ double rhs_at(const StepParams& P, const Stencil& st, int l, int d) {
+__device__ __forceinline__ double rhs_at(const double* __restrict__ G, double alphaG, const double* __restrict__ Xp,
+                                         const Stencil& st, int l, int d, int ld) {
   double acc = 0.0;
-  if (P.alphaG != 0.0) acc = P.alphaG * __ldg(P.G + addr<DIR>(l, d, P.ld));
+  if (alphaG != 0.0) acc = alphaG * __ldg(G + addr<DIR>(l, d, ld));
 #pragma unroll
   for (int q = 0; q < 7; ++q)
-    if (st.idx[q] >= 0) acc += st.w[q] * __ldg(P.Xp + addr<DIR>(st.idx[q], d, P.ld));
+    if (st.idx[q] >= 0) acc += st.w[q] * __ldg(Xp + addr<DIR>(st.idx[q], d, ld));
   return acc;
+}
+
+/* Line processing order of the y-solve (lines = rows): rows that are
+ * x-neighbours in the apply stencil (same x-element, degrees k, k+-2) are
+ * processed back to back so their W rows are reused from L2; hat rows last. */
+__device__ __forceinline__ int row_of(const DirDev& o, int lp) {
+  const int nb = o.nb, q = o.p - 1;
+  if (lp >= nb) return lp - nb;
+  const int e = lp / q, k = lp - e * q;
+  return o.nh + k * o.n + e;
 }
 
 template <int DIR>
@@ -266,18 +278,20 @@ __device__ __forceinline__ bool thread_coords(const StepParams& P, int& l, int& 
     l = blockIdx.x * blockDim.x + threadIdx.x;
     e = blockIdx.y % n;
     pi = blockIdx.y / n;
-  } else {
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    e = (int)(idx % n);
-    pi = (int)((idx / n) & 1);
-    l = (int)(idx / (2 * n));
+    return l < P.o.N;
   }
-  return l < P.o.N;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  e = (int)(idx % n);
+  pi = (int)((idx / n) & 1);
+  const int lp = (int)(idx / (2 * n));
+  if (lp >= P.o.N) return false;
+  l = row_of(P.o, lp);
+  return true;
 }
 
-/* K2/K3/K4: fused apply + element-local bubble chain solve, chain in registers */
+/* K2/K3/K4, register variant: chain kept in registers (CL <= 64). */
 template <int DIR, int CL>
-__global__ void __launch_bounds__(128) k_bubbles(StepParams P) {
+__global__ void __launch_bounds__(128) k_bubbles_reg(StepParams P) {
   int l, e, pi;
   if (!thread_coords<DIR>(P, l, e, pi)) return;
   const DirDev& s = P.s;
@@ -288,8 +302,7 @@ __global__ void __launch_bounds__(128) k_bubbles(StepParams P) {
   double r[CL];
 #pragma unroll
   for (int c = 0; c < CL; ++c)
-    if (c < m) r[c] = rhs_at<DIR>(P, st, l, s.nh + (pi + 2 * c) * s.n + e);
-  // L^T y = r (descending), then L z = y (ascending): z = D_e^{-1} r on this chain
+    if (c < m) r[c] = rhs_at<DIR>(P.G, P.alphaG, P.Xp, st, l, s.nh + (pi + 2 * c) * s.n + e, P.ld);
   const double* __restrict__ il = P.f.il;
   const double* __restrict__ g = P.f.g;
   double y = 0.0;
@@ -311,9 +324,15 @@ __global__ void __launch_bounds__(128) k_bubbles(StepParams P) {
     }
 }
 
-/* long chains (> 64): y staged through the output array (L2 round trip) */
-template <int DIR>
-__global__ void __launch_bounds__(128) k_bubbles_long(StepParams P) {
+/* K2/K3/K4, streaming variant (default): the apply is evaluated on the
+ * loads while the chain is swept from its top degree down (L^T y = r), y is
+ * parked in the output array -- at this occupancy the round trip stays in
+ * L2 (~(resident chains) x 8m bytes << 126 MB), so DRAM sees one write --
+ * and the ascending sweep (L z = y) overwrites it with z = D_e^{-1} r.
+ * Loads are batched U chain positions at a time for memory-level
+ * parallelism; ~70 registers instead of ~170. */
+template <int DIR, int U>
+__global__ void __launch_bounds__(256) k_bubbles(StepParams P) {
   int l, e, pi;
   if (!thread_coords<DIR>(P, l, e, pi)) return;
   const DirDev& s = P.s;
@@ -321,73 +340,157 @@ __global__ void __launch_bounds__(128) k_bubbles_long(StepParams P) {
   if (m == 0) return;
   Stencil st;
   stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+  const double* __restrict__ G = P.G;
+  const double* __restrict__ Xp = P.Xp;
   const double* __restrict__ il = P.f.il;
   const double* __restrict__ g = P.f.g;
+  double* __restrict__ out = P.out;
+  const double aG = P.alphaG;
+  const int n = s.n, nh = s.nh, ld = P.ld;
   double y = 0.0;
-#pragma unroll 8
-  for (int c = m - 1; c >= 0; --c) {
-    const int b = (pi + 2 * c) * s.n + e;
-    const double r = rhs_at<DIR>(P, st, l, s.nh + b);
-    y = (r - __ldg(g + b) * y) * __ldg(il + b);
-    P.out[addr<DIR>(l, s.nh + b, P.ld)] = y;
+  for (int c0 = m - 1; c0 >= 0; c0 -= U) {
+    double r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 - u;
+      r[u] = c >= 0 ? rhs_at<DIR>(G, aG, Xp, st, l, nh + (pi + 2 * c) * n + e, ld) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 - u;
+      if (c >= 0) {
+        const int b = (pi + 2 * c) * n + e;
+        y = (r[u] - __ldg(g + b) * y) * __ldg(il + b);
+        out[addr<DIR>(l, nh + b, ld)] = y;
+      }
+    }
   }
   double z = 0.0, gp = 0.0;
-#pragma unroll 8
-  for (int c = 0; c < m; ++c) {
-    const int b = (pi + 2 * c) * s.n + e;
-    double* o = P.out + addr<DIR>(l, s.nh + b, P.ld);
-    z = (*o - gp * z) * __ldg(il + b);
-    gp = __ldg(g + b);
-    *o = z;
+  for (int c0 = 0; c0 < m; c0 += U) {
+    double yy[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u;
+      yy[u] = c < m ? out[addr<DIR>(l, nh + (pi + 2 * c) * n + e, ld)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u;
+      if (c < m) {
+        const int b = (pi + 2 * c) * n + e;
+        z = (yy[u] - gp * z) * __ldg(il + b);
+        gp = __ldg(g + b);
+        out[addr<DIR>(l, nh + b, ld)] = z;
+      }
+    }
   }
 }
 
-/* K5: per line, hat RHS r_h - B z and the hat tridiagonal solve */
-template <int DIR>
-__global__ void __launch_bounds__(128) k_hats(StepParams P) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= P.o.N) return;
+/* K5: hat right-hand side r_h - B z for a tile of LB lines (parallel over
+ * hats), then the hat tridiagonal reverse-Cholesky solve of each line from
+ * shared memory, then the write-back.  smem: [nh][LB] doubles. */
+template <int DIR, int LB>
+__global__ void __launch_bounds__(256) k_hats(StepParams P) {
+  extern __shared__ double sh[];
   const DirDev& s = P.s;
-  if (s.nh == 0) return;
-  Stencil st;
-  stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+  const int nh = s.nh, ld = P.ld, n = s.n;
+  const int l0 = blockIdx.x * LB;
   const double S = P.f.sig;
   const bool k1 = s.p - 2 >= 1;
-  double y = 0.0;
-  for (int t = s.nh - 1; t >= 0; --t) {
-    double rh = rhs_at<DIR>(P, st, l, t);
+  const double* __restrict__ G = P.G;
+  const double* __restrict__ Xp = P.Xp;
+  const double* __restrict__ out_r = P.out;
+  // phase A: rh(l, t)
+  auto rhs_hat = [&](const Stencil& st, int l, int t) {
+    double rh = rhs_at<DIR>(G, P.alphaG, Xp, st, l, t, ld);
     const int node = node_of_hat(t, s.bc);
     const int eL = node - 1, eR = node;
     if (eL >= 0) {
       const double dl = s.delta[eL];
-      rh -= s_hat_bub(S, dl, 1, 0) * P.out[addr<DIR>(l, s.nh + eL, P.ld)];
-      if (k1) rh -= s_hat_bub(S, dl, 1, 1) * P.out[addr<DIR>(l, s.nh + s.n + eL, P.ld)];
+      rh -= s_hat_bub(S, dl, 1, 0) * out_r[addr<DIR>(l, nh + eL, ld)];
+      if (k1) rh -= s_hat_bub(S, dl, 1, 1) * out_r[addr<DIR>(l, nh + n + eL, ld)];
     }
-    if (eR <= s.n - 1) {
+    if (eR <= n - 1) {
       const double dr = s.delta[eR];
-      rh -= s_hat_bub(S, dr, 0, 0) * P.out[addr<DIR>(l, s.nh + eR, P.ld)];
-      if (k1) rh -= s_hat_bub(S, dr, 0, 1) * P.out[addr<DIR>(l, s.nh + s.n + eR, P.ld)];
+      rh -= s_hat_bub(S, dr, 0, 0) * out_r[addr<DIR>(l, nh + eR, ld)];
+      if (k1) rh -= s_hat_bub(S, dr, 0, 1) * out_r[addr<DIR>(l, nh + n + eR, ld)];
     }
-    y = (rh - __ldg(P.f.gh + t) * y) * __ldg(P.f.ilh + t);
-    P.out[addr<DIR>(l, t, P.ld)] = y;
+    return rh;
+  };
+  if (DIR == 0) {
+    // lines = columns: lane -> column (coalesced), thread groups over t
+    const int j = threadIdx.x % LB, tg = threadIdx.x / LB, ng = blockDim.x / LB;
+    const int l = l0 + j;
+    if (l < P.o.N) {
+      Stencil st;
+      stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+      for (int t = tg; t < nh; t += ng) sh[t * LB + j] = rhs_hat(st, l, t);
+    }
+  } else {
+    // lines = rows: a warp per row, lanes over the contiguous hat columns
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = w; j < LB; j += nw) {
+      const int lp = l0 + j;
+      if (lp >= P.o.N) break;
+      const int l = row_of(P.o, lp);
+      Stencil st;
+      stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+      for (int t = lane; t < nh; t += 32) sh[t * LB + j] = rhs_hat(st, l, t);
+    }
   }
-  double x = 0.0, gp = 0.0;
-  for (int t = 0; t < s.nh; ++t) {
-    double* o = P.out + addr<DIR>(l, t, P.ld);
-    x = (*o - gp * x) * __ldg(P.f.ilh + t);
-    gp = __ldg(P.f.gh + t);
-    *o = x;
+  __syncthreads();
+  // phase B: sequential tridiagonal solve per line, in shared memory
+  if (threadIdx.x < LB && l0 + (int)threadIdx.x < P.o.N) {
+    const int j = threadIdx.x;
+    const double* __restrict__ ilh = P.f.ilh;
+    const double* __restrict__ gh = P.f.gh;
+    double y = 0.0;
+    for (int t = nh - 1; t >= 0; --t) {
+      y = (sh[t * LB + j] - __ldg(gh + t) * y) * __ldg(ilh + t);
+      sh[t * LB + j] = y;
+    }
+    double x = 0.0, gp = 0.0;
+    for (int t = 0; t < nh; ++t) {
+      x = (sh[t * LB + j] - gp * x) * __ldg(ilh + t);
+      gp = __ldg(gh + t);
+      sh[t * LB + j] = x;
+    }
+  }
+  __syncthreads();
+  // phase C: write back
+  if (DIR == 0) {
+    const int j = threadIdx.x % LB, tg = threadIdx.x / LB, ng = blockDim.x / LB;
+    const int l = l0 + j;
+    if (l < P.o.N)
+      for (int t = tg; t < nh; t += ng) P.out[addr<DIR>(l, t, ld)] = sh[t * LB + j];
+  } else {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = w; j < LB; j += nw) {
+      const int lp = l0 + j;
+      if (lp >= P.o.N) break;
+      const int l = row_of(P.o, lp);
+      for (int t = lane; t < nh; t += 32) P.out[addr<DIR>(l, t, ld)] = sh[t * LB + j];
+    }
   }
 }
 
+static int bubble_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HPFEM_BUBBLE_KERNEL");
+    v = (e && e[0] == 'r') ? 1 : 0;  // "reg" selects the register variant
+  }
+  return v;
+}
+
 template <int DIR, int CL>
-static cudaError_t launch_bub(const StepParams& P, cudaStream_t st) {
+static cudaError_t launch_bub_reg(const StepParams& P, cudaStream_t st) {
   if (DIR == 0) {
     dim3 grid((P.o.N + 127) / 128, P.s.n * 2);
-    k_bubbles<DIR, CL><<<grid, 128, 0, st>>>(P);
+    k_bubbles_reg<DIR, CL><<<grid, 128, 0, st>>>(P);
   } else {
     const long long nthr = (long long)P.o.N * 2 * P.s.n;
-    k_bubbles<DIR, CL><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(P);
+    k_bubbles_reg<DIR, CL><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(P);
   }
   return cudaGetLastError();
 }
@@ -395,17 +498,20 @@ static cudaError_t launch_bub(const StepParams& P, cudaStream_t st) {
 template <int DIR>
 static cudaError_t launch_bub_dir(const StepParams& P, cudaStream_t st) {
   const int m = chain_len(P.s.p, 0);
-  if (m <= 4) return launch_bub<DIR, 4>(P, st);
-  if (m <= 8) return launch_bub<DIR, 8>(P, st);
-  if (m <= 16) return launch_bub<DIR, 16>(P, st);
-  if (m <= 32) return launch_bub<DIR, 32>(P, st);
-  if (m <= 64) return launch_bub<DIR, 64>(P, st);
+  if (bubble_variant() == 1 && m <= 64) {
+    if (m <= 4) return launch_bub_reg<DIR, 4>(P, st);
+    if (m <= 8) return launch_bub_reg<DIR, 8>(P, st);
+    if (m <= 16) return launch_bub_reg<DIR, 16>(P, st);
+    if (m <= 32) return launch_bub_reg<DIR, 32>(P, st);
+    return launch_bub_reg<DIR, 64>(P, st);
+  }
+  constexpr int U = 8;
   if (DIR == 0) {
-    dim3 grid((P.o.N + 127) / 128, P.s.n * 2);
-    k_bubbles_long<DIR><<<grid, 128, 0, st>>>(P);
+    dim3 grid((P.o.N + 255) / 256, P.s.n * 2);
+    k_bubbles<DIR, U><<<grid, 256, 0, st>>>(P);
   } else {
     const long long nthr = (long long)P.o.N * 2 * P.s.n;
-    k_bubbles_long<DIR><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(P);
+    k_bubbles<DIR, U><<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(P);
   }
   return cudaGetLastError();
 }
@@ -414,14 +520,23 @@ cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st) {
   return P.dir == 0 ? launch_bub_dir<0>(P, st) : launch_bub_dir<1>(P, st);
 }
 
+template <int DIR>
+static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
+  constexpr int LB = 32;
+  const size_t smem = sizeof(double) * (size_t)P.s.nh * LB;
+  static size_t opted = 48 * 1024;
+  if (smem > opted) {
+    cudaError_t e = cudaFuncSetAttribute(k_hats<DIR, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    opted = smem;
+  }
+  k_hats<DIR, LB><<<(P.o.N + LB - 1) / LB, 256, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st) {
   if (P.s.nh == 0) return cudaSuccess;
-  const unsigned grid = (P.o.N + 127) / 128;
-  if (P.dir == 0)
-    k_hats<0><<<grid, 128, 0, st>>>(P);
-  else
-    k_hats<1><<<grid, 128, 0, st>>>(P);
-  return cudaGetLastError();
+  return P.dir == 0 ? launch_hats_dir<0>(P, st) : launch_hats_dir<1>(P, st);
 }
 
 /* K6: U(i, b) = z(i, b) - vL(b) x_h(i, hL) - vR(b) x_h(i, hR) along rows */
