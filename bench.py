@@ -269,7 +269,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
 
     # ---- device-resident timed region (profiling events on the same stream)
-    plan.profile((6 * J + 16) * args.steps + 64)
+    plan.profile((12 * J + 32) * args.steps + 64)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(gpu_id_for(dev)) as clk:
         barrier()

@@ -36,6 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     headers = glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(HERE, "..", "include", "hpfem.h")]
     plan_o = os.path.join(OBJ, "plan.o")
     kern_o = os.path.join(OBJ, "kernels.o")
+    tma_o = os.path.join(OBJ, "tma_step.o")
     out = None if verbose else subprocess.DEVNULL
     if force or _stale(plan_o, [os.path.join(CSRC, "plan.cpp")] + headers):
         subprocess.check_call(["g++", *CXX_FLAGS, "-c", os.path.join(CSRC, "plan.cpp"), "-o", plan_o])
@@ -44,9 +45,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with open(log, "w") as fh:
             subprocess.check_call([NVCC, *NVCC_FLAGS, "-c", os.path.join(CSRC, "kernels.cu"), "-o", kern_o],
                                   stdout=fh, stderr=subprocess.STDOUT)
-    if force or _stale(LIB, [plan_o, kern_o]):
+    if force or _stale(tma_o, [os.path.join(CSRC, "tma_step.cu")] + headers):
+        log = os.path.join(OBJ, "ptxas_tma.log")
+        with open(log, "w") as fh:
+            subprocess.check_call([NVCC, *NVCC_FLAGS, "-c", os.path.join(CSRC, "tma_step.cu"), "-o", tma_o],
+                                  stdout=fh, stderr=subprocess.STDOUT)
+    if force or _stale(LIB, [plan_o, kern_o, tma_o]):
         tmp = LIB + f".tmp{os.getpid()}"
-        subprocess.check_call([NVCC, "-shared", *ARCH, plan_o, kern_o, "-o", tmp, "-lquadmath"], stdout=out)
+        subprocess.check_call([NVCC, "-shared", *ARCH, plan_o, kern_o, tma_o, "-o", tmp, "-lquadmath"], stdout=out)
         os.replace(tmp, LIB)
     return LIB
 

@@ -7,6 +7,8 @@
 
 #include <cuda_runtime.h>
 
+#include "ops1d.h"
+
 namespace hpfem {
 
 /* one 1D direction as seen by the device */
@@ -25,7 +27,15 @@ struct DirDev {
  *   il[b], g[b]  : chain reverse-Cholesky diag^{-1} and sub-diagonal, b = k n + e
  *   vL[b], vR[b] : D_e^{-1} B^T e_{hL(e)}, D_e^{-1} B^T e_{hR(e)} (static condensation)
  *   ilh[t], gh[t]: reverse Cholesky of the hat Schur complement A0 - B D^{-1} B^T
- * stored contiguously: [il | g | vL | vR | ilh | gh], stride = 4 nb + 2 nh (+pad). */
+ *   cf           : chain-major copy for the TMA kernels, chain (e, pi) at
+ *                  cf + (2e + pi) * cfs, position c at [3c] = il_c,
+ *                  [3c+1] = g_c il_c, [3c+2] = g_{c-1} il_c, so that each
+ *                  recurrence step is one dependent FMA:
+ *                    y_c = il_c r_c - (g_c il_c) y_{c+1},
+ *                    z_c = il_c y_c - (g_{c-1} il_c) z_{c-1};
+ *                  cfs = 3 chain_len(p, 0) rounded up to even, + 2 (spreads
+ *                  smem banks); one contiguous block per tile.
+ * stored contiguously: [il | g | vL | vR | ilh | gh | cf], 256-byte aligned. */
 struct FacView {
   const double* il;
   const double* g;
@@ -33,11 +43,20 @@ struct FacView {
   const double* vR;
   const double* ilh;
   const double* gh;
+  const double* cf;
+  int cfs;
   double kap, sig;
 };
 
-inline size_t fac_stride(const DirDev& d) {
+HD int fac_cfs(const DirDev& d) { return ((3 * (d.p / 2) + 1) & ~1) + 2; }
+
+HD size_t fac_cf_off(const DirDev& d) {
   size_t s = 4 * (size_t)d.nb + 2 * (size_t)d.nh;
+  return (s + 31) & ~(size_t)31;
+}
+
+inline size_t fac_stride(const DirDev& d) {
+  size_t s = fac_cf_off(d) + (size_t)d.n * 2 * fac_cfs(d);
   return (s + 31) & ~(size_t)31;  // 256-byte aligned sets
 }
 
@@ -49,9 +68,39 @@ inline FacView fac_view(const DirDev& d, const double* base, double kap, double 
   f.vR = base + 3 * (size_t)d.nb;
   f.ilh = base + 4 * (size_t)d.nb;
   f.gh = base + 4 * (size_t)d.nb + d.nh;
+  f.cf = base + fac_cf_off(d);
+  f.cfs = fac_cfs(d);
   f.kap = kap;
   f.sig = sig;
   return f;
+}
+
+/* Internal (plan-owned) 2D array layout: row i = x-dof (unpadded), row
+ * stride ld doubles, y-hats at columns 0..nh_y-1 and the y-bubbles from
+ * column hb on, either
+ *   degree-major  (emaj = 0): bubble (k, e) at hb + k np + e   (lanes over
+ *                 elements coalesce: the LDG kernels), or
+ *   element-major (emaj = 1): bubble (k, e) at hb + e Q + k    (a group of
+ *                 whole elements is one contiguous run: the TMA kernels).
+ * hb, np, Q and ld are even so every block starts on a 16-byte boundary
+ * (DESIGN.md §5). */
+struct Layout {
+  int ld;
+  int hb;
+  int np;
+  int Q;
+  int emaj;
+};
+
+inline Layout make_layout(const DirDev& y, int emaj) {
+  Layout L;
+  L.hb = (y.nh + 1) & ~1;
+  L.np = (y.n + 1) & ~1;
+  L.Q = (y.p - 1 + 1) & ~1;
+  L.emaj = emaj;
+  L.ld = emaj ? L.hb + y.n * L.Q : L.hb + (y.p - 1) * L.np;
+  if (L.ld < 2) L.ld = 2;
+  return L;
 }
 
 /* cross-line stencil mode of a half-step kernel */
@@ -65,7 +114,9 @@ enum StencilMode { ST_NONE = 0, ST_APPLY = 1, ST_CORR = 2 };
  * solve along o to the true iterate: x_b = z_b - vL x_hL - vR x_hR. */
 struct StepParams {
   int dir;  // 0: solve along x (lines = columns), 1: along y (lines = rows)
-  int ld;   // N_y
+  int ld;   // internal row stride (Layout.ld)
+  Layout lay;
+  int lp_begin, lp_count;  // lines processed, in processing order (see row_of)
   DirDev s, o;
   const double* G;
   double alphaG;
@@ -83,8 +134,10 @@ cudaError_t launch_factor(const DirDev& d, const double* kap, const double* sig,
                           size_t stride, int* err, cudaStream_t st);
 cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st);
 cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st);
-cudaError_t launch_correct_rows(const DirDev& y, int Nx, const double* vL, const double* vR, double* U,
-                                cudaStream_t st);
+cudaError_t launch_copyin(const DirDev& x, const DirDev& y, const Layout& L, const double* G, double* Gp,
+                          cudaStream_t st);
+cudaError_t launch_finalize(const DirDev& x, const DirDev& y, const Layout& L, const double* vL, const double* vR,
+                            const double* X, double* U, cudaStream_t st);
 cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const double* U, double* F,
                            cudaStream_t st);
 cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st);

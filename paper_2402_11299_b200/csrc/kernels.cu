@@ -77,6 +77,17 @@ __global__ void k_factor_chains(DirDev d, const double* __restrict__ kap, const 
     g[b] = gc;
     lnext = l;
   }
+  {  // chain-major (il, g il, g_prev il) for the TMA kernels
+    double* cf = base + fac_cf_off(d) + (size_t)(2 * e + pi) * fac_cfs(d);
+    double gprev = 0.0;
+    for (int c = 0; c < m; ++c) {
+      const int b = (pi + 2 * c) * d.n + e;
+      cf[3 * c] = il[b];
+      cf[3 * c + 1] = g[b] * il[b];
+      cf[3 * c + 2] = gprev * il[b];
+      gprev = g[b];
+    }
+  }
   // v_side = T^{-1} (beta e_0): the chain-first bubble is the only one
   // coupled to the hats (W_0 / W_1, ops1d.h)
   for (int side = 0; side < 2; ++side) {
@@ -243,10 +254,28 @@ __device__ __forceinline__ void stencil_build(const DirDev& o, int l, int mode, 
   }
 }
 
-/* address of (line l, dof d) for a solve along DIR */
+/* internal column of y-dof d */
+__host__ __device__ __forceinline__ int ycol_ke(const Layout& L, int k, int e) {
+  return L.emaj ? L.hb + e * L.Q + k : L.hb + k * L.np + e;
+}
+__host__ __device__ __forceinline__ int ycol(const Layout& L, const DirDev& y, int d) {
+  if (d < y.nh) return d;
+  const int b = d - y.nh, k = b / y.n;
+  return ycol_ke(L, k, b - k * y.n);
+}
+
+/* Address of (line l, dof position d) for a solve along DIR, both already in
+ * internal coordinates: DIR 0 -> l is a column, d a row; DIR 1 -> l is a
+ * row, d a column. */
 template <int DIR>
 __device__ __forceinline__ size_t addr(int l, int d, int ld) {
   return DIR == 0 ? (size_t)d * ld + l : (size_t)l * ld + d;
+}
+
+/* internal position of the solve-direction dof (bubble (k, e) or hat t) */
+template <int DIR>
+__device__ __forceinline__ int spos_bub(const StepParams& P, int k, int e) {
+  return DIR == 0 ? P.s.nh + k * P.s.n + e : ycol_ke(P.lay, k, e);
 }
 
 /* r(l, d) = alphaG G(l,d) + sum_q w_q Xp(idx_q, d)   (read-only inputs) */
@@ -271,38 +300,60 @@ __device__ __forceinline__ int row_of(const DirDev& o, int lp) {
   return o.nh + k * o.n + e;
 }
 
+/* line dof index (in direction o) of processing position lp */
 template <int DIR>
-__device__ __forceinline__ bool thread_coords(const StepParams& P, int& l, int& e, int& pi) {
-  const int n = P.s.n;
+__device__ __forceinline__ int line_dof(const StepParams& P, int lp) {
+  return DIR == 0 ? lp : row_of(P.o, lp);
+}
+
+/* Stencil for line l (a dof of direction o) with its indices mapped to
+ * internal coordinates (columns for DIR 0, rows for DIR 1). */
+template <int DIR>
+__device__ __forceinline__ void line_stencil(const StepParams& P, int l, Stencil& st) {
+  stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
   if (DIR == 0) {
-    l = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < 7; ++q)
+      if (st.idx[q] >= 0) st.idx[q] = ycol(P.lay, P.o, st.idx[q]);
+  }
+}
+
+/* thread -> (internal line coordinate li, line dof l, element e, parity pi) */
+template <int DIR>
+__device__ __forceinline__ bool thread_coords(const StepParams& P, int& li, int& l, int& e, int& pi) {
+  const int n = P.s.n;
+  int lp;
+  if (DIR == 0) {
+    lp = blockIdx.x * blockDim.x + threadIdx.x;
     e = blockIdx.y % n;
     pi = blockIdx.y / n;
-    return l < P.o.N;
+  } else {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    e = (int)(idx % n);
+    pi = (int)((idx / n) & 1);
+    lp = (int)(idx / (2 * n));
   }
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  e = (int)(idx % n);
-  pi = (int)((idx / n) & 1);
-  const int lp = (int)(idx / (2 * n));
-  if (lp >= P.o.N) return false;
-  l = row_of(P.o, lp);
+  if (lp >= P.lp_count) return false;
+  lp += P.lp_begin;
+  l = line_dof<DIR>(P, lp);
+  li = DIR == 0 ? ycol(P.lay, P.o, l) : l;
   return true;
 }
 
 /* K2/K3/K4, register variant: chain kept in registers (CL <= 64). */
 template <int DIR, int CL>
 __global__ void __launch_bounds__(128) k_bubbles_reg(StepParams P) {
-  int l, e, pi;
-  if (!thread_coords<DIR>(P, l, e, pi)) return;
+  int li, l, e, pi;
+  if (!thread_coords<DIR>(P, li, l, e, pi)) return;
   const DirDev& s = P.s;
   const int m = chain_len(s.p, pi);
   if (m == 0) return;
   Stencil st;
-  stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+  line_stencil<DIR>(P, l, st);
   double r[CL];
 #pragma unroll
   for (int c = 0; c < CL; ++c)
-    if (c < m) r[c] = rhs_at<DIR>(P.G, P.alphaG, P.Xp, st, l, s.nh + (pi + 2 * c) * s.n + e, P.ld);
+    if (c < m) r[c] = rhs_at<DIR>(P.G, P.alphaG, P.Xp, st, li, spos_bub<DIR>(P, pi + 2 * c, e), P.ld);
   const double* __restrict__ il = P.f.il;
   const double* __restrict__ g = P.f.g;
   double y = 0.0;
@@ -320,7 +371,7 @@ __global__ void __launch_bounds__(128) k_bubbles_reg(StepParams P) {
       const int b = (pi + 2 * c) * s.n + e;
       z = (r[c] - gp * z) * __ldg(il + b);
       gp = __ldg(g + b);
-      P.out[addr<DIR>(l, s.nh + b, P.ld)] = z;
+      P.out[addr<DIR>(li, spos_bub<DIR>(P, pi + 2 * c, e), P.ld)] = z;
     }
 }
 
@@ -333,27 +384,27 @@ __global__ void __launch_bounds__(128) k_bubbles_reg(StepParams P) {
  * parallelism; ~70 registers instead of ~170. */
 template <int DIR, int U>
 __global__ void __launch_bounds__(256) k_bubbles(StepParams P) {
-  int l, e, pi;
-  if (!thread_coords<DIR>(P, l, e, pi)) return;
+  int li, l, e, pi;
+  if (!thread_coords<DIR>(P, li, l, e, pi)) return;
   const DirDev& s = P.s;
   const int m = chain_len(s.p, pi);
   if (m == 0) return;
   Stencil st;
-  stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+  line_stencil<DIR>(P, l, st);
   const double* __restrict__ G = P.G;
   const double* __restrict__ Xp = P.Xp;
   const double* __restrict__ il = P.f.il;
   const double* __restrict__ g = P.f.g;
   double* __restrict__ out = P.out;
   const double aG = P.alphaG;
-  const int n = s.n, nh = s.nh, ld = P.ld;
+  const int n = s.n, ld = P.ld;
   double y = 0.0;
   for (int c0 = m - 1; c0 >= 0; c0 -= U) {
     double r[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int c = c0 - u;
-      r[u] = c >= 0 ? rhs_at<DIR>(G, aG, Xp, st, l, nh + (pi + 2 * c) * n + e, ld) : 0.0;
+      r[u] = c >= 0 ? rhs_at<DIR>(G, aG, Xp, st, li, spos_bub<DIR>(P, pi + 2 * c, e), ld) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -361,7 +412,7 @@ __global__ void __launch_bounds__(256) k_bubbles(StepParams P) {
       if (c >= 0) {
         const int b = (pi + 2 * c) * n + e;
         y = (r[u] - __ldg(g + b) * y) * __ldg(il + b);
-        out[addr<DIR>(l, nh + b, ld)] = y;
+        out[addr<DIR>(li, spos_bub<DIR>(P, pi + 2 * c, e), ld)] = y;
       }
     }
   }
@@ -371,7 +422,7 @@ __global__ void __launch_bounds__(256) k_bubbles(StepParams P) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int c = c0 + u;
-      yy[u] = c < m ? out[addr<DIR>(l, nh + (pi + 2 * c) * n + e, ld)] : 0.0;
+      yy[u] = c < m ? out[addr<DIR>(li, spos_bub<DIR>(P, pi + 2 * c, e), ld)] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -380,7 +431,7 @@ __global__ void __launch_bounds__(256) k_bubbles(StepParams P) {
         const int b = (pi + 2 * c) * n + e;
         z = (yy[u] - gp * z) * __ldg(il + b);
         gp = __ldg(g + b);
-        out[addr<DIR>(l, nh + b, ld)] = z;
+        out[addr<DIR>(li, spos_bub<DIR>(P, pi + 2 * c, e), ld)] = z;
       }
     }
   }
@@ -394,26 +445,25 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
   extern __shared__ double sh[];
   const DirDev& s = P.s;
   const int nh = s.nh, ld = P.ld, n = s.n;
-  const int l0 = blockIdx.x * LB;
+  const int l0 = blockIdx.x * LB;  // first line (processing position) of the tile
   const double S = P.f.sig;
   const bool k1 = s.p - 2 >= 1;
   const double* __restrict__ G = P.G;
   const double* __restrict__ Xp = P.Xp;
   const double* __restrict__ out_r = P.out;
-  // phase A: rh(l, t)
-  auto rhs_hat = [&](const Stencil& st, int l, int t) {
-    double rh = rhs_at<DIR>(G, P.alphaG, Xp, st, l, t, ld);
+  auto rhs_hat = [&](const Stencil& st, int li, int t) {
+    double rh = rhs_at<DIR>(G, P.alphaG, Xp, st, li, t, ld);
     const int node = node_of_hat(t, s.bc);
     const int eL = node - 1, eR = node;
     if (eL >= 0) {
       const double dl = s.delta[eL];
-      rh -= s_hat_bub(S, dl, 1, 0) * out_r[addr<DIR>(l, nh + eL, ld)];
-      if (k1) rh -= s_hat_bub(S, dl, 1, 1) * out_r[addr<DIR>(l, nh + n + eL, ld)];
+      rh -= s_hat_bub(S, dl, 1, 0) * out_r[addr<DIR>(li, spos_bub<DIR>(P, 0, eL), ld)];
+      if (k1) rh -= s_hat_bub(S, dl, 1, 1) * out_r[addr<DIR>(li, spos_bub<DIR>(P, 1, eL), ld)];
     }
     if (eR <= n - 1) {
       const double dr = s.delta[eR];
-      rh -= s_hat_bub(S, dr, 0, 0) * out_r[addr<DIR>(l, nh + eR, ld)];
-      if (k1) rh -= s_hat_bub(S, dr, 0, 1) * out_r[addr<DIR>(l, nh + n + eR, ld)];
+      rh -= s_hat_bub(S, dr, 0, 0) * out_r[addr<DIR>(li, spos_bub<DIR>(P, 0, eR), ld)];
+      if (k1) rh -= s_hat_bub(S, dr, 0, 1) * out_r[addr<DIR>(li, spos_bub<DIR>(P, 1, eR), ld)];
     }
     return rh;
   };
@@ -423,8 +473,9 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
     const int l = l0 + j;
     if (l < P.o.N) {
       Stencil st;
-      stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
-      for (int t = tg; t < nh; t += ng) sh[t * LB + j] = rhs_hat(st, l, t);
+      line_stencil<DIR>(P, l, st);
+      const int li = ycol(P.lay, P.o, l);
+      for (int t = tg; t < nh; t += ng) sh[t * LB + j] = rhs_hat(st, li, t);
     }
   } else {
     // lines = rows: a warp per row, lanes over the contiguous hat columns
@@ -434,12 +485,12 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
       if (lp >= P.o.N) break;
       const int l = row_of(P.o, lp);
       Stencil st;
-      stencil_build(P.o, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+      line_stencil<DIR>(P, l, st);
       for (int t = lane; t < nh; t += 32) sh[t * LB + j] = rhs_hat(st, l, t);
     }
   }
   __syncthreads();
-  // phase B: sequential tridiagonal solve per line, in shared memory
+  // sequential tridiagonal reverse-Cholesky solve per line, in shared memory
   if (threadIdx.x < LB && l0 + (int)threadIdx.x < P.o.N) {
     const int j = threadIdx.x;
     const double* __restrict__ ilh = P.f.ilh;
@@ -457,12 +508,13 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
     }
   }
   __syncthreads();
-  // phase C: write back
   if (DIR == 0) {
     const int j = threadIdx.x % LB, tg = threadIdx.x / LB, ng = blockDim.x / LB;
     const int l = l0 + j;
-    if (l < P.o.N)
-      for (int t = tg; t < nh; t += ng) P.out[addr<DIR>(l, t, ld)] = sh[t * LB + j];
+    if (l < P.o.N) {
+      const int li = ycol(P.lay, P.o, l);
+      for (int t = tg; t < nh; t += ng) P.out[addr<DIR>(li, t, ld)] = sh[t * LB + j];
+    }
   } else {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int j = w; j < LB; j += nw) {
@@ -486,10 +538,10 @@ static int bubble_variant() {
 template <int DIR, int CL>
 static cudaError_t launch_bub_reg(const StepParams& P, cudaStream_t st) {
   if (DIR == 0) {
-    dim3 grid((P.o.N + 127) / 128, P.s.n * 2);
+    dim3 grid((P.lp_count + 127) / 128, P.s.n * 2);
     k_bubbles_reg<DIR, CL><<<grid, 128, 0, st>>>(P);
   } else {
-    const long long nthr = (long long)P.o.N * 2 * P.s.n;
+    const long long nthr = (long long)P.lp_count * 2 * P.s.n;
     k_bubbles_reg<DIR, CL><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(P);
   }
   return cudaGetLastError();
@@ -507,16 +559,17 @@ static cudaError_t launch_bub_dir(const StepParams& P, cudaStream_t st) {
   }
   constexpr int U = 8;
   if (DIR == 0) {
-    dim3 grid((P.o.N + 255) / 256, P.s.n * 2);
+    dim3 grid((P.lp_count + 255) / 256, P.s.n * 2);
     k_bubbles<DIR, U><<<grid, 256, 0, st>>>(P);
   } else {
-    const long long nthr = (long long)P.o.N * 2 * P.s.n;
+    const long long nthr = (long long)P.lp_count * 2 * P.s.n;
     k_bubbles<DIR, U><<<(unsigned)((nthr + 255) / 256), 256, 0, st>>>(P);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st) {
+  if (P.lp_count <= 0) return cudaSuccess;
   return P.dir == 0 ? launch_bub_dir<0>(P, st) : launch_bub_dir<1>(P, st);
 }
 
@@ -539,25 +592,49 @@ cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st) {
   return P.dir == 0 ? launch_hats_dir<0>(P, st) : launch_hats_dir<1>(P, st);
 }
 
-/* K6: U(i, b) = z(i, b) - vL(b) x_h(i, hL) - vR(b) x_h(i, hR) along rows */
-__global__ void k_correct_rows(DirDev y, int Nx, const double* __restrict__ vL, const double* __restrict__ vR,
-                               double* __restrict__ U) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+/* K6: U = W_J C^{-1} materialised in the caller's layout:
+ * U(i, j) = X(i, col j) for hats, z - vL x_hL - vR x_hR for bubbles (the
+ * deferred correction of the final y-solve). */
+__global__ void __launch_bounds__(256) k_finalize(DirDev y, int Nx, Layout L, const double* __restrict__ vL,
+                                                   const double* __restrict__ vR, const double* __restrict__ X,
+                                                   double* __restrict__ U) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
-  if (b >= y.nb || i >= Nx) return;
-  const int e = b % y.n;
-  const int hL = hat_of_node(e, y.n, y.bc), hR = hat_of_node(e + 1, y.n, y.bc);
-  double* row = U + (size_t)i * y.N;
-  double v = row[y.nh + b];
-  if (hL >= 0) v -= __ldg(vL + b) * row[hL];
-  if (hR >= 0) v -= __ldg(vR + b) * row[hR];
-  row[y.nh + b] = v;
+  if (j >= y.N || i >= Nx) return;
+  const double* row = X + (size_t)i * L.ld;
+  double v;
+  if (j < y.nh) {
+    v = row[j];
+  } else {
+    const int b = j - y.nh, k = b / y.n, e = b - k * y.n;
+    const int hL = hat_of_node(e, y.n, y.bc), hR = hat_of_node(e + 1, y.n, y.bc);
+    v = row[ycol_ke(L, k, e)];
+    if (hL >= 0) v -= __ldg(vL + b) * row[hL];
+    if (hR >= 0) v -= __ldg(vR + b) * row[hR];
+  }
+  U[(size_t)i * y.N + j] = v;
 }
 
-cudaError_t launch_correct_rows(const DirDev& y, int Nx, const double* vL, const double* vR, double* U,
-                                cudaStream_t st) {
-  dim3 grid((y.nb + 255) / 256, Nx);
-  k_correct_rows<<<grid, 256, 0, st>>>(y, Nx, vL, vR, U);
+cudaError_t launch_finalize(const DirDev& x, const DirDev& y, const Layout& L, const double* vL, const double* vR,
+                            const double* X, double* U, cudaStream_t st) {
+  dim3 grid((y.N + 255) / 256, x.N);
+  k_finalize<<<grid, 256, 0, st>>>(y, x.N, L, vL, vR, X, U);
+  return cudaGetLastError();
+}
+
+/* G (caller layout) -> Gp (internal layout) */
+__global__ void __launch_bounds__(256) k_copyin(DirDev y, int Nx, Layout L, const double* __restrict__ G,
+                                                 double* __restrict__ Gp) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= y.N || i >= Nx) return;
+  Gp[(size_t)i * L.ld + ycol(L, y, j)] = __ldg(G + (size_t)i * y.N + j);
+}
+
+cudaError_t launch_copyin(const DirDev& x, const DirDev& y, const Layout& L, const double* G, double* Gp,
+                          cudaStream_t st) {
+  dim3 grid((y.N + 255) / 256, x.N);
+  k_copyin<<<grid, 256, 0, st>>>(y, x.N, L, G, Gp);
   return cudaGetLastError();
 }
 

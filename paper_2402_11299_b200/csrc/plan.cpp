@@ -16,6 +16,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -23,6 +24,7 @@
 #include "../../include/hpfem.h"
 #include "hpfem_internal.h"
 #include "ops1d.h"
+#include "tma_step.h"
 
 using namespace hpfem;
 
@@ -253,7 +255,12 @@ struct hpfem_plan_s {
   double* d_delta = nullptr;      // [n_x | n_y]
   double* d_shift = nullptr;      // kap/sig arrays
   int* d_err = nullptr;
-  double* work = nullptr;         // N_x x N_y
+  Layout lay{};                   // internal padded layout (hpfem_internal.h)
+  double* Gp = nullptr;           // internal copy of G
+  double* X1 = nullptr;           // W_{j-1/2} (deferred along y), final y-solve
+  double* X2 = nullptr;           // W_j (deferred along x)
+  TmaPlan* tma = nullptr;         // TMA tensor maps over {Gp, X1, X2} (null = LDG kernels only)
+  bool use_tma = false;           // TMA half-step kernels + element-major layout
   long long launches = 0;
   // profiling (hpfem_plan_profile)
   std::vector<cudaEvent_t> ev;
@@ -291,12 +298,15 @@ void prof_add(hpfem_plan_t pl, int kind, int e0, int e1, double bytes) {
 void free_plan(hpfem_plan_t pl) {
   if (!pl) return;
   free_events(pl);
+  tma_plan_destroy(pl->tma);
   cudaFree(pl->fx);
   cudaFree(pl->fy);
   cudaFree(pl->d_delta);
   cudaFree(pl->d_shift);
   cudaFree(pl->d_err);
-  cudaFree(pl->work);
+  cudaFree(pl->Gp);
+  cudaFree(pl->X1);
+  cudaFree(pl->X2);
   delete pl;
 }
 
@@ -395,8 +405,21 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   if ((ce = cudaMemsetAsync(pl->fx, 0, sizeof(double) * pl->sx * J, st)) != cudaSuccess) return fail_cuda(ce, "memset");
   if ((ce = cudaMemsetAsync(pl->fy, 0, sizeof(double) * pl->sy * (J + 1), st)) != cudaSuccess)
     return fail_cuda(ce, "memset");
-  if ((ce = cudaMalloc(&pl->work, sizeof(double) * (size_t)hx.N * hy.N)) != cudaSuccess)
-    return fail_cuda(ce, "alloc workspace");
+  {
+    const char* no_tma = std::getenv("HPFEM_NO_TMA");
+    pl->use_tma = !(no_tma && no_tma[0] == '1') && tma_shape_ok(pl->dx, pl->dy);
+  }
+  pl->lay = make_layout(pl->dy, pl->use_tma ? 1 : 0);
+  {
+    const size_t bytes = sizeof(double) * ((size_t)hx.N * pl->lay.ld + 64);  // +slack for bulk copies
+    for (double** b : {&pl->Gp, &pl->X1, &pl->X2}) {
+      if ((ce = cudaMalloc(b, bytes)) != cudaSuccess) return fail_cuda(ce, "alloc workspace");
+      if ((ce = cudaMemsetAsync(*b, 0, bytes, st)) != cudaSuccess) return fail_cuda(ce, "memset workspace");
+    }
+    double* const arrays[3] = {pl->Gp, pl->X1, pl->X2};
+    pl->tma = tma_plan_create(pl->dx, pl->dy, pl->lay, arrays, pl->use_tma);
+    if (pl->use_tma && !tma_supports(pl->tma, 0)) return fail_cuda(cudaErrorNotSupported, "TMA tensor maps");
+  }
   const double* dsh = pl->d_shift;
   if ((ce = launch_factor(pl->dx, dsh, dsh + (J + 1), J, pl->fx, pl->sx, pl->d_err, st)) != cudaSuccess)
     return fail_cuda(ce, "factor x");
@@ -435,24 +458,42 @@ bool overlap(const void* a, const void* b, size_t bytes) {
   return x < y + bytes && y < x + bytes;
 }
 
-/* One line-solve pass (bubble kernel + hat kernel).  Algorithmic bytes:
- * per dof read G (if used), read the previous iterate (if any), write the
- * output. */
-int run_step(hpfem_plan_t pl, const StepParams& P, cudaStream_t st, bool final_step) {
+/* One line-solve pass.  Bubble lines: the TMA kernel when the shape allows
+ * (else the LDG kernel); hat lines of the other direction: the LDG kernel;
+ * then the hat solve.  Algorithmic bytes per dof: read G (if used), read the
+ * previous iterate (if any), write the output.
+ * ia_g / ia_w: which of {Gp, X1, X2} are G and Xp (-1 = unused). */
+int run_step(hpfem_plan_t pl, StepParams P, cudaStream_t st, bool final_step, int ia_g, int ia_w) {
   const double per = 8.0 * ((P.alphaG != 0.0 ? 1 : 0) + (P.mode != ST_NONE ? 1 : 0) + 1);
   const int k0 = final_step ? 2 : 0, k1 = final_step ? 2 : 1;
+  int rc;
   const int e0 = prof_mark(pl, st);
-  int rc = count_launch(pl, launch_step_bubbles(P, st), "bubble kernel");
-  if (rc) return rc;
-  const int e1 = prof_mark(pl, st);
-  prof_add(pl, k0, e0, e1, per * (double)P.o.N * P.s.nb);
+  if (tma_supports(pl->tma, P.dir)) {
+    rc = count_launch(pl, tma_launch_step(pl->tma, P, ia_g, ia_w, st), "TMA bubble kernel");
+    if (rc) return rc;
+    const int e1 = prof_mark(pl, st);
+    prof_add(pl, k0, e0, e1, per * (double)P.o.nb * P.s.nb);
+    // the other direction's hat lines
+    StepParams H = P;
+    H.lp_begin = P.dir == 0 ? 0 : P.o.nb;
+    H.lp_count = P.o.nh;
+    if (H.lp_count > 0) {
+      rc = count_launch(pl, launch_step_bubbles(H, st), "hat-line bubble kernel");
+      if (rc) return rc;
+      prof_add(pl, k1, e1, prof_mark(pl, st), per * (double)P.o.nh * P.s.nb);
+    }
+  } else {
+    rc = count_launch(pl, launch_step_bubbles(P, st), "bubble kernel");
+    if (rc) return rc;
+    prof_add(pl, k0, e0, prof_mark(pl, st), per * (double)P.o.N * P.s.nb);
+  }
   if (P.s.nh > 0) {
+    const int e2 = prof_mark(pl, st);
     rc = count_launch(pl, launch_step_hats(P, st), "hat kernel");
     if (rc) return rc;
-    const int e2 = prof_mark(pl, st);
-    prof_add(pl, k1, e1, e2, per * (double)P.o.N * P.s.nh);
+    prof_add(pl, k1, e2, prof_mark(pl, st), per * (double)P.o.N * P.s.nh);
   }
-  return rc;
+  return HPFEM_OK;
 }
 
 }  // namespace
@@ -510,74 +551,76 @@ int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, vo
   if (overlap(F, U, bytes)) return set_err(HPFEM_EINVAL, "F and U overlap");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   pl->launches = 0;
+  if (iters == 0) {  // W_0 = 0
+    cudaError_t ce = cudaMemsetAsync(U, 0, bytes, st);
+    return ce == cudaSuccess ? HPFEM_OK : cuda_err(ce, "memset");
+  }
   const double hw2 = 0.5 * pl->omega * pl->omega;
-  double* X1 = U;          // W_{j-1/2} (deferred along y), then U
-  double* X2 = pl->work;   // W_j      (deferred along x)
   int rc;
+  {
+    const int e0 = prof_mark(pl, st);
+    if ((rc = count_launch(pl, launch_copyin(pl->dx, pl->dy, pl->lay, F, pl->Gp, st), "copy-in"))) return rc;
+    prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);  // layout change, not algorithmic
+  }
+  auto base = [&](int dir) {
+    StepParams P{};
+    P.dir = dir;
+    P.ld = pl->lay.ld;
+    P.lay = pl->lay;
+    P.s = dir == 0 ? pl->dx : pl->dy;
+    P.o = dir == 0 ? pl->dy : pl->dx;
+    P.lp_begin = 0;
+    P.lp_count = P.o.N;
+    return P;
+  };
   for (int j = 0; j < iters; ++j) {
     // half-step A: W_{j-1/2} = (G - (A_x - p_j M_x) W_{j-1}) (A_y + p_j M_y)^{-1}
-    StepParams A{};
-    A.dir = 1;
-    A.ld = pl->hy.N;
-    A.s = pl->dy;
-    A.o = pl->dx;
-    A.G = F;
+    StepParams A = base(1);
+    A.G = pl->Gp;
     A.alphaG = 1.0;
     A.f = fview(pl, 1, j);
-    A.out = X1;
+    A.out = pl->X1;
     if (j == 0) {
       A.mode = ST_NONE;  // W_0 = 0
     } else {
       const FacView prev = fview(pl, 0, j - 1);
       A.mode = ST_APPLY;
-      A.Xp = X2;
+      A.Xp = pl->X2;
       A.kap_a = 1.0;
       A.tau = hw2 - pl->P[j];
       A.cvL = prev.vL;
       A.cvR = prev.vR;
     }
-    if ((rc = run_step(pl, A, st, false))) return rc;
+    if ((rc = run_step(pl, A, st, false, 0, j == 0 ? -1 : 2))) return rc;
     // half-step B: W_j = (A_x - q_j M_x)^{-1} (G - W_{j-1/2} (A_y + q_j M_y))
-    StepParams B{};
-    B.dir = 0;
-    B.ld = pl->hy.N;
-    B.s = pl->dx;
-    B.o = pl->dy;
-    B.G = F;
+    StepParams B = base(0);
+    B.G = pl->Gp;
     B.alphaG = 1.0;
     B.f = fview(pl, 0, j);
-    B.out = X2;
+    B.out = pl->X2;
     B.mode = ST_APPLY;
-    B.Xp = X1;
+    B.Xp = pl->X1;
     B.kap_a = 1.0;
     B.tau = hw2 + pl->Q[j];
     B.cvL = A.f.vL;
     B.cvR = A.f.vR;
-    if ((rc = run_step(pl, B, st, false))) return rc;
+    if ((rc = run_step(pl, B, st, false, 0, 1))) return rc;
   }
-  if (iters == 0) {
-    cudaError_t ce = cudaMemsetAsync(U, 0, bytes, st);
-    return ce == cudaSuccess ? HPFEM_OK : cuda_err(ce, "memset");
-  }
-  // RETURN W_J C^{-1}: y-solves with the mass factor, then materialise
-  StepParams Fin{};
-  Fin.dir = 1;
-  Fin.ld = pl->hy.N;
-  Fin.s = pl->dy;
-  Fin.o = pl->dx;
+  // RETURN W_J C^{-1}: y-solves with the mass factor, then materialise U
+  StepParams Fin = base(1);
   Fin.G = nullptr;
   Fin.alphaG = 0.0;
   Fin.f = fview(pl, 1, pl->J);
-  Fin.out = X1;
+  Fin.out = pl->X1;
   Fin.mode = ST_CORR;
-  Fin.Xp = X2;
+  Fin.Xp = pl->X2;
   const FacView last = fview(pl, 0, iters - 1);
   Fin.cvL = last.vL;
   Fin.cvR = last.vR;
-  if ((rc = run_step(pl, Fin, st, true))) return rc;
+  if ((rc = run_step(pl, Fin, st, true, -1, 2))) return rc;
   const int e0 = prof_mark(pl, st);
-  rc = count_launch(pl, launch_correct_rows(pl->dy, pl->hx.N, Fin.f.vL, Fin.f.vR, U, st), "correct kernel");
-  prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);  // not algorithmic: the deferred correction pass
+  rc = count_launch(pl, launch_finalize(pl->dx, pl->dy, pl->lay, Fin.f.vL, Fin.f.vR, pl->X1, U, st), "finalize");
+  prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);
   return rc;
 }
 

@@ -1,0 +1,824 @@
+/*
+ * tma_step.cu -- TMA-fed, warp-specialised persistent half-step kernels
+ * (K2-K4 for the bubble lines) for sm_100a.
+ *
+ * One ADI half-step (Alg. 2) = for every line: evaluate the
+ * cross-line sparse apply of the other direction on the previous iterate,
+ * then solve the element-local bubble chains (static condensation of the
+ * reverse-Cholesky solve, Cor. 4.3 P:L600-L614 / P:L636-L638).
+ *
+ * Data movement: one elected producer thread streams the tiles a CTA needs
+ * from HBM into a ring of shared-memory stages with cp.async.bulk.tensor
+ * (TMA), completion tracked by mbarriers; eight consumer warps evaluate the
+ * stencil from shared memory (each W value is fetched once per CTA and reused
+ * by the 3-5 lines that need it) and run the chain recurrences with the
+ * chain held in registers.  The producer runs ahead across tile boundaries
+ * (persistent CTAs), so HBM stays busy while the consumers do the upward
+ * sweep and the stores of a finished tile.
+ *
+ *  x-solve (DIR 0, lines = y-bubble columns):  tile = (x-element e_x,
+ *    x-parity, a group of EG0 y-elements); stage c = one row d_c of the x-chain:
+ *    G and W boxes [p_y-1][EG0] of the 3D view (e_y, k_y, row) plus the few
+ *    y-hat columns the tile's stencils touch.  The y-stencil (k_y, k_y +- 2,
+ *    hats) lies entirely inside the tile: no halo.
+ *  y-solve (DIR 1, lines = x-bubble rows):  tile = (x-element e_x, x-parity,
+ *    R consecutive rows of that x-chain, a group of EG1 y-elements); stage c =
+ *    chain position c (y-degrees 2c, 2c+1): G box [R][2][EG1], W box
+ *    [R+2][2][EG1] (the x-stencil rows k_x-2 .. k_x+2R of the same x-chain)
+ *    and the two x-hat rows of e_x.  W rows are reused R/(R+2) from smem.
+ *
+ * Hat lines (n+-1 of them) are left to the LDG kernel of kernels.cu.
+ */
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
+#include "hpfem_internal.h"
+#include "ops1d.h"
+#include "tma_step.h"
+
+namespace hpfem {
+
+/* ------------------------------------------------------------------ */
+/* PTX helpers: mbarrier + TMA                                         */
+/* ------------------------------------------------------------------ */
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(su32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(su32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(su32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+/* the cross-line stencil (same construction as kernels.cu), device copy */
+struct Sten5 {
+  double w[5];  // weights of [l, l-2n, l+2n, hL, hR] (0 where absent)
+};
+
+__device__ __forceinline__ void sten5_build(const DirDev& o, int l, int mode, double kap, double tau,
+                                            const double* __restrict__ cvL, const double* __restrict__ cvR,
+                                            Sten5& st) {
+  // l is a bubble dof (k, e) of direction o
+  const int n = o.n, b = l - o.nh, k = b / n, e = b - k * n;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) st.w[q] = 0.0;
+  const bool hL = hat_of_node(e, n, o.bc) >= 0, hR = hat_of_node(e + 1, n, o.bc) >= 0;
+  if (mode == ST_CORR) {
+    st.w[0] = 1.0;
+    if (hL && cvL) st.w[3] = -cvL[b];
+    if (hR && cvR) st.w[4] = -cvR[b];
+    return;
+  }
+  if (mode != ST_APPLY) return;
+  const double dl = o.delta[e];
+  const bool hm = k >= 2, hp = k + 2 <= o.p - 2;
+  const double sd = s_bub_diag(kap, tau, dl, k);
+  const double sm = hm ? s_bub_off(tau, dl, k - 2) : 0.0;
+  const double sp = hp ? s_bub_off(tau, dl, k) : 0.0;
+  double cL = s_hat_bub(tau, dl, 0, k), cR = s_hat_bub(tau, dl, 1, k);
+  if (cvL) {
+    cL -= sd * cvL[b];
+    if (hm) cL -= sm * cvL[b - 2 * n];
+    if (hp) cL -= sp * cvL[b + 2 * n];
+  }
+  if (cvR) {
+    cR -= sd * cvR[b];
+    if (hm) cR -= sm * cvR[b - 2 * n];
+    if (hp) cR -= sp * cvR[b + 2 * n];
+  }
+  st.w[0] = -sd;
+  st.w[1] = -sm;
+  st.w[2] = -sp;
+  st.w[3] = hL ? -cL : 0.0;
+  st.w[4] = hR ? -cR : 0.0;
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map), "r"(c0),
+      "r"(c1), "r"(c2), "r"(c3), "r"(su32(src))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct TmaStepArgs {
+  StepParams P;
+  int EG;           // y-elements per tile
+  int R;            // rows per tile (y-solve)
+  int ntiles;
+  int nstages;
+  int stage_bytes;  // bytes per ring stage (all boxes, 128-aligned)
+  int off_w, off_h; // byte offsets of the W and hat boxes inside a stage
+  int tx_bytes;     // bytes the TMA delivers per stage
+  int hw;           // hat box width (x-solve)
+  int out_off;      // y-solve: byte offset of the two output staging buffers
+  int fac_off;      // byte offset of the two per-tile factor buffers
+  int fac_doubles;  // doubles per factor buffer
+};
+
+constexpr int NT = 256;    // threads per CTA; thread 0 doubles as the TMA producer
+constexpr int NW = NT / 32;
+constexpr int KR = 8;      // x-solve: chain positions (rows) per stage
+constexpr int KCP = 8;     // y-solve: chain positions per stage (16 degrees)
+constexpr int KBOX = 18;   // y-solve: degrees per box row (16 + 2 to spread smem banks)
+
+struct Producer {
+  int tile, s;    // next stage to produce: tile and stage index within it (descending)
+  uint32_t it;    // its sequence number
+  uint32_t tt;    // tiles started (selects the factor buffer)
+  bool first;     // the next stage is the first of its tile
+};
+
+/* ------------------------------------------------------------------ */
+/* x-solve (DIR 0), element-major layout                               */
+/* tile = (x-element e_x, x-parity pi, group of EG y-elements); stage  */
+/* s = chain positions [KR s, KR s + KR) of the x-chain (rows)         */
+/* ------------------------------------------------------------------ */
+template <int MODE>
+__device__ __forceinline__ void x_produce(const TmaStepArgs& A, Producer& pr, unsigned char* ring, uint64_t* full,
+                                          uint64_t* empty, const CUtensorMap* mG0, const CUtensorMap* mG1,
+                                          const CUtensorMap* mW0, const CUtensorMap* mW1, const CUtensorMap* mH0,
+                                          const CUtensorMap* mH1, double* fbuf, uint64_t* fempty) {
+  const StepParams& P = A.P;
+  const DirDev& x = P.s;
+  const DirDev& y = P.o;
+  const int NST = A.nstages, EG = A.EG;
+  const int ngroups = (y.n + EG - 1) / EG;
+  if (pr.tile >= A.ntiles) return;
+  const int g = pr.tile % ngroups, rest = pr.tile / ngroups;
+  const int e_x = rest % x.n, pi = rest / x.n;
+  const int col0 = P.lay.hb + g * EG * P.lay.Q;
+  const int h0 = (y.bc == 0 ? g * EG - 1 : g * EG) & ~1;  // innermost TMA coordinate: 16-byte aligned
+  const int slot = pr.it % NST;
+  if (pr.it >= (uint32_t)NST) mbar_wait(&empty[slot], ((pr.it / NST) - 1) & 1);
+  unsigned char* st = ring + (size_t)slot * A.stage_bytes;
+  if (pr.first) {  // the tile's chain factors ride with its first stage
+    const uint32_t fb = pr.tt & 1;
+    if (pr.tt >= 2) mbar_wait(&fempty[fb], ((pr.tt >> 1) - 1) & 1);
+    const uint32_t fbytes = P.f.cfs * 8;
+    mbar_expect_tx(&full[slot], A.tx_bytes + fbytes);
+    bulk_load(fbuf + fb * A.fac_doubles, P.f.cf + (size_t)(2 * e_x + pi) * P.f.cfs, fbytes, &full[slot]);
+  } else {
+    mbar_expect_tx(&full[slot], A.tx_bytes);
+  }
+  const CUtensorMap* mG = pi ? mG1 : mG0;
+  const CUtensorMap* mW = pi ? mW1 : mW0;
+  if (MODE != ST_CORR) tma_load_3d(st, mG, &full[slot], col0, e_x, KR * pr.s);
+  if (MODE != ST_NONE) {
+    tma_load_3d(st + A.off_w, mW, &full[slot], col0, e_x, KR * pr.s);
+    tma_load_3d(st + A.off_h, pi ? mH1 : mH0, &full[slot], h0, e_x, KR * pr.s);
+  }
+  ++pr.it;
+  pr.first = false;
+  if (--pr.s < 0) {
+    pr.tile += gridDim.x;
+    ++pr.tt;
+    pr.first = true;
+    if (pr.tile < A.ntiles) pr.s = (chain_len(x.p, (pr.tile / ngroups) / x.n) - 1) / KR;
+  }
+}
+
+template <int CL, int MODE>
+__global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const __grid_constant__ CUtensorMap mG0,
+                                                     const __grid_constant__ CUtensorMap mG1,
+                                                     const __grid_constant__ CUtensorMap mW0,
+                                                     const __grid_constant__ CUtensorMap mW1,
+                                                     const __grid_constant__ CUtensorMap mH0,
+                                                     const __grid_constant__ CUtensorMap mH1) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const StepParams& P = A.P;
+  const DirDev& x = P.s;  // solve direction
+  const DirDev& y = P.o;  // apply direction
+  const int NST = A.nstages;
+  unsigned char* ring = smem_raw;
+  double* fbuf = reinterpret_cast<double*>(smem_raw + A.fac_off);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.fac_off + 2 * A.fac_doubles * sizeof(double));
+  uint64_t* empty = full + NST;
+  uint64_t* fempty = empty + NST;
+  const int lane = threadIdx.x & 31;
+  const int EG = A.EG, q = y.p - 1, Q = P.lay.Q, BW = EG * Q;
+  const int ngroups = (y.n + EG - 1) / EG;
+  Producer pr;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NST; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], NW);
+    }
+    mbar_init(&fempty[0], NW);
+    mbar_init(&fempty[1], NW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    pr.tile = blockIdx.x;
+    pr.it = 0;
+    pr.tt = 0;
+    pr.first = true;
+    pr.s = pr.tile < A.ntiles ? (chain_len(x.p, (pr.tile / ngroups) / x.n) - 1) / KR : -1;
+    for (int k = 0; k < NST; ++k) x_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf, fempty);
+  }
+  const int tid = threadIdx.x;
+  const int eo = tid / Q, ky = tid - eo * Q;
+  uint32_t it = 0, ctt = 0;
+  for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++ctt) {
+    const int g = tile % ngroups, rest = tile / ngroups;
+    const int e_x = rest % x.n, pi = rest / x.n;
+    const int e0 = g * EG, ey = e0 + eo;
+    const int m = chain_len(x.p, pi);
+    const double* fb = fbuf + (ctt & 1) * A.fac_doubles;  // [3c] il, [3c+1] g il, [3c+2] g_prev il
+    const bool valid = eo < EG && ky < q && ey < y.n;
+    const int h0 = (y.bc == 0 ? e0 - 1 : e0) & ~1;
+    Sten5 st;
+    int o0 = 0, o1 = 0, o2 = 0, o3 = 0, o4 = 0;
+    if (valid) {
+      sten5_build(y, y.nh + ky * y.n + ey, MODE, P.kap_a, P.tau, P.cvL, P.cvR, st);
+      o0 = eo * Q + ky;
+      o1 = eo * Q + (ky >= 2 ? ky - 2 : ky);
+      o2 = eo * Q + (ky + 2 < q ? ky + 2 : ky);
+      const int hl = hat_of_node(ey, y.n, y.bc), hr = hat_of_node(ey + 1, y.n, y.bc);
+      o3 = (hl >= 0 ? hl : h0 + 1) - h0;
+      o4 = (hr >= 0 ? hr : h0 + 1) - h0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) st.w[k] = 0.0;
+    }
+    double ys[CL];
+    double yv = 0.0;
+#pragma unroll
+    for (int sg = CL / KR - 1; sg >= 0; --sg) {
+      if (KR * sg < m) {
+        const int slot = it % NST;
+        mbar_wait(&full[slot], (it / NST) & 1);
+        const unsigned char* stg = ring + (size_t)slot * A.stage_bytes;
+        double rv[KR];
+#pragma unroll
+        for (int kk = 0; kk < KR; ++kk) {
+          const double* Gs = reinterpret_cast<const double*>(stg) + kk * BW;
+          const double* Ws = reinterpret_cast<const double*>(stg + A.off_w) + kk * BW;
+          const double* Hs = reinterpret_cast<const double*>(stg + A.off_h) + kk * A.hw;
+          double r = 0.0;
+          if (MODE != ST_CORR) r = Gs[o0];
+          if (MODE != ST_NONE)
+            r += st.w[0] * Ws[o0] + st.w[1] * Ws[o1] + st.w[2] * Ws[o2] + st.w[3] * Hs[o3] + st.w[4] * Hs[o4];
+          rv[kk] = r;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        ++it;
+        if (threadIdx.x == 0) x_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf, fempty);
+#pragma unroll
+        for (int kk = KR - 1; kk >= 0; --kk) {
+          const int c = KR * sg + kk;
+          if (c < m) {
+            yv = fma(-fb[3 * c + 1], yv, fb[3 * c] * rv[kk]);
+            ys[c] = yv;
+          }
+        }
+      }
+    }
+    if (valid) {
+      double* __restrict__ out = P.out + P.lay.hb + (size_t)ey * Q + ky;
+      double z = 0.0;
+#pragma unroll
+      for (int c = 0; c < CL; ++c) {
+        if (c < m) {
+          z = fma(-fb[3 * c + 2], z, fb[3 * c] * ys[c]);
+          out[(size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld] = z;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&fempty[ctt & 1]);
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* y-solve (DIR 1), element-major layout                               */
+/* tile = (x-element e_x, x-parity, window of R rows of that x-chain,  */
+/* group of EG y-elements); stage s = y-chain positions [8s, 8s+8)     */
+/* ------------------------------------------------------------------ */
+struct YTile {
+  int e_x, pi, kw, g;
+};
+
+__device__ __forceinline__ YTile y_decode(const TmaStepArgs& A, int tile) {
+  const DirDev& y = A.P.s;
+  const DirDev& x = A.P.o;
+  const int ngroups = (y.n + A.EG - 1) / A.EG;
+  const int nw0 = (chain_len(x.p, 0) + A.R - 1) / A.R, nw1 = (chain_len(x.p, 1) + A.R - 1) / A.R;
+  YTile t;
+  t.g = tile % ngroups;
+  const int rest = tile / ngroups;
+  t.e_x = rest / (nw0 + nw1);
+  const int w = rest % (nw0 + nw1);
+  t.pi = w < nw0 ? 0 : 1;
+  t.kw = t.pi == 0 ? w : w - nw0;
+  return t;
+}
+
+template <int MODE>
+__device__ __forceinline__ void y_produce(const TmaStepArgs& A, Producer& pr, unsigned char* ring, uint64_t* full,
+                                          uint64_t* empty, const CUtensorMap* mG0, const CUtensorMap* mG1,
+                                          const CUtensorMap* mW0, const CUtensorMap* mW1, const CUtensorMap* mH,
+                                          double* fbuf, uint64_t* fempty) {
+  const DirDev& y = A.P.s;
+  const DirDev& x = A.P.o;
+  const int NST = A.nstages;
+  if (pr.tile >= A.ntiles) return;
+  const YTile t = y_decode(A, pr.tile);
+  const int e0 = t.g * A.EG, kh0 = t.kw * A.R;
+  const int hL = x.bc == 0 ? t.e_x - 1 : t.e_x;
+  const int slot = pr.it % NST;
+  if (pr.it >= (uint32_t)NST) mbar_wait(&empty[slot], ((pr.it / NST) - 1) & 1);
+  unsigned char* st = ring + (size_t)slot * A.stage_bytes;
+  if (pr.first) {  // chain factors of the tile's EG elements x 2 parities (one contiguous block)
+    const uint32_t fb = pr.tt & 1;
+    if (pr.tt >= 2) mbar_wait(&fempty[fb], ((pr.tt >> 1) - 1) & 1);
+    const int ne = (y.n - e0) < A.EG ? (y.n - e0) : A.EG;
+    const uint32_t fbytes = 2 * ne * A.P.f.cfs * 8;
+    mbar_expect_tx(&full[slot], A.tx_bytes + fbytes);
+    bulk_load(fbuf + fb * A.fac_doubles, A.P.f.cf + (size_t)(2 * e0) * A.P.f.cfs, fbytes, &full[slot]);
+  } else {
+    mbar_expect_tx(&full[slot], A.tx_bytes);
+  }
+  const int k0 = 2 * KCP * pr.s;
+  if (MODE != ST_CORR) tma_load_4d(st, t.pi ? mG1 : mG0, &full[slot], k0, e0, t.e_x, kh0);
+  if (MODE != ST_NONE) {
+    tma_load_4d(st + A.off_w, t.pi ? mW1 : mW0, &full[slot], k0, e0, t.e_x, kh0 - 1);
+    tma_load_3d(st + A.off_h, mH, &full[slot], k0, e0, hL);
+  }
+  ++pr.it;
+  pr.first = false;
+  if (--pr.s < 0) {
+    pr.tile += gridDim.x;
+    ++pr.tt;
+    pr.first = true;
+    pr.s = (chain_len(y.p, 0) - 1) / KCP;
+  }
+}
+
+template <int CL, int MODE>
+__global__ void __launch_bounds__(NT, 1)
+    k_ystep_tma(const TmaStepArgs A, const __grid_constant__ CUtensorMap mG0, const __grid_constant__ CUtensorMap mG1,
+                const __grid_constant__ CUtensorMap mW0, const __grid_constant__ CUtensorMap mW1,
+                const __grid_constant__ CUtensorMap mH, const __grid_constant__ CUtensorMap mO0,
+                const __grid_constant__ CUtensorMap mO1) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const StepParams& P = A.P;
+  const DirDev& y = P.s;  // solve direction
+  const DirDev& x = P.o;  // apply direction
+  const int NST = A.nstages;
+  unsigned char* ring = smem_raw;
+  double* obuf = reinterpret_cast<double*>(smem_raw + A.out_off);  // 2 x NW x [RW][EG][16]
+  double* fbuf = reinterpret_cast<double*>(smem_raw + A.fac_off);   // 2 x [EG][2][cfs]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.fac_off + 2 * A.fac_doubles * sizeof(double));
+  uint64_t* empty = full + NST;
+  uint64_t* fempty = empty + NST;
+  const int lane = threadIdx.x & 31;
+  const int EG = A.EG, R = A.R;
+  const int my = chain_len(y.p, 0);
+  const int nst_tile = (my - 1) / KCP + 1;
+  Producer pr;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NST; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], NW);
+    }
+    mbar_init(&fempty[0], NW);
+    mbar_init(&fempty[1], NW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    pr.tile = blockIdx.x;
+    pr.it = 0;
+    pr.tt = 0;
+    pr.first = true;
+    pr.s = nst_tile - 1;
+    for (int k = 0; k < NST; ++k) y_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH, fbuf, fempty);
+  }
+  // thread -> (row r of the window, y-parity py, y-element eo)
+  const int tid = threadIdx.x;
+  const int eo = tid % EG, py = (tid / EG) & 1, r = tid / (2 * EG);
+  const int cfs = P.f.cfs;
+  uint32_t it = 0, ctt = 0;
+  int ob = 0;  // output staging buffer parity
+  for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++ctt) {
+    const YTile t = y_decode(A, tile);
+    const double* fb = fbuf + (ctt & 1) * A.fac_doubles + (eo * 2 + py) * cfs;  // this thread's chain
+    const int e_x = t.e_x, pi = t.pi;
+    const int e0 = t.g * EG, ey = e0 + eo;
+    const int kx = pi + 2 * (t.kw * R + r);
+    const int mthr = chain_len(y.p, py);
+    const bool valid = r < R && kx <= x.p - 2 && ey < y.n;
+    Sten5 st;
+    if (valid) {
+      sten5_build(x, x.nh + kx * x.n + e_x, MODE, P.kap_a, P.tau, P.cvL, P.cvR, st);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) st.w[k] = 0.0;
+    }
+    const int rr = r < R ? r : 0;
+    const int og = (rr * EG + eo) * KBOX + py;          // G box [R][EG][KBOX]
+    const int ow1 = (rr * EG + eo) * KBOX + py;         // W box [R+2][EG][KBOX]: row k_x - 2
+    const int ow0 = ((rr + 1) * EG + eo) * KBOX + py;   //   k_x
+    const int ow2 = ((rr + 2) * EG + eo) * KBOX + py;   //   k_x + 2
+    const int oh0 = eo * KBOX + py;                     // hat box [2][EG][KBOX]: hL
+    const int oh1 = (EG + eo) * KBOX + py;              //   hR
+    double ys[CL];
+    double yv = 0.0;
+#pragma unroll
+    for (int sg = CL / KCP - 1; sg >= 0; --sg) {
+      if (KCP * sg < my) {
+        const int slot = it % NST;
+        mbar_wait(&full[slot], (it / NST) & 1);
+        const unsigned char* stg = ring + (size_t)slot * A.stage_bytes;
+        const double* Gs = reinterpret_cast<const double*>(stg);
+        const double* Ws = reinterpret_cast<const double*>(stg + A.off_w);
+        const double* Hs = reinterpret_cast<const double*>(stg + A.off_h);
+        double rv[KCP];
+#pragma unroll
+        for (int u = 0; u < KCP; ++u) {
+          double v = 0.0;
+          if (MODE != ST_CORR) v = Gs[og + 2 * u];
+          if (MODE != ST_NONE)
+            v += st.w[0] * Ws[ow0 + 2 * u] + st.w[1] * Ws[ow1 + 2 * u] + st.w[2] * Ws[ow2 + 2 * u] +
+                 st.w[3] * Hs[oh0 + 2 * u] + st.w[4] * Hs[oh1 + 2 * u];
+          rv[u] = v;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        ++it;
+        if (threadIdx.x == 0) y_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH, fbuf, fempty);
+#pragma unroll
+        for (int u = KCP - 1; u >= 0; --u) {
+          const int c = KCP * sg + u;
+          if (c < mthr) {
+            yv = fma(-fb[3 * c + 1], yv, fb[3 * c] * rv[u]);
+            ys[c] = yv;
+          }
+        }
+      }
+    }
+    // upward sweep, staged per warp through shared memory and stored with TMA
+    // per 16 degrees (one box of this warp's RW rows; no CTA-wide barrier)
+    double z = 0.0;
+    const int RW = 16 / EG;            // rows per warp (EG is a power of two <= 8)
+    const int wr0 = (tid >> 5) * RW;   // first row of this warp
+#pragma unroll
+    for (int sg = 0; sg < CL / KCP; ++sg) {
+      if (KCP * sg < my) {
+        double* o = obuf + ((size_t)ob * NW + (tid >> 5)) * (32 * 8);  // [RW][EG][16] = 256 doubles
+        if (lane == 0) bulk_wait_read<1>();  // the store that last used this buffer has read it
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < KCP; ++u) {
+          const int c = KCP * sg + u;
+          double zv = 0.0;
+          if (valid && c < mthr) {
+            z = fma(-fb[3 * c + 2], z, fb[3 * c] * ys[c]);
+            zv = z;
+          }
+          o[((r - wr0) * EG + eo) * 16 + py + 2 * u] = zv;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && wr0 < R) {
+          tma_store_4d(pi ? &mO1 : &mO0, o, 2 * KCP * sg, e0, e_x, t.kw * R + wr0);
+          bulk_commit();
+        }
+        ob ^= 1;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&fempty[ctt & 1]);
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+/* ------------------------------------------------------------------ */
+/* host side: tensor maps and launch                                   */
+/* ------------------------------------------------------------------ */
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+static bool encode(CUtensorMap* m, int rank, void* base, const uint64_t* dims, const uint64_t* strides_bytes,
+                   const uint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i < rank - 1) s[i] = strides_bytes[i];
+  }
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base, d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct TmaPlan {
+  bool ok = false;
+  int EG0 = 0, EG1 = 0, R = 0, hw = 0;
+  int sms = 148;
+  // per internal array a (0 = Gp, 1 = X1, 2 = X2)
+  CUtensorMap xv[3][4];                 // x-solve views per array: [pi] bubble boxes, [2+pi] hat boxes
+  CUtensorMap yG[3][2], yW[3][2], yH[3];
+  CUtensorMap yO[2];                    // y-solve output stores (X1), per parity
+};
+
+static int even_up(int v) { return (v + 1) & ~1; }
+
+/* y-solve tile shape: EG y-elements (a power of two <= 8, so that a warp
+ * holds whole rows: RW = 16/EG rows per warp) x R rows of an x-chain (a
+ * multiple of RW, with the R+2-row W box inside each parity's row count) */
+static void y_tile_shape(const DirDev& x, const DirDev& y, int& EG, int& R) {
+  EG = 8;
+  while (EG > y.n) EG >>= 1;
+  const int RW = 16 / EG;
+  R = NT / (2 * EG);
+  if (R > chain_len(x.p, 1) - 2) R = chain_len(x.p, 1) - 2;
+  R -= R % RW;
+}
+
+/* shape conditions of the TMA path (both directions, element-major layout) */
+bool tma_shape_ok(const DirDev& x, const DirDev& y) {
+  const int Q = even_up(y.p - 1);
+  int EG, R;
+  y_tile_shape(x, y, EG, R);
+  return x.nb > 0 && y.nb > 0 && x.N >= 2 && Q <= 256 && Q >= KBOX && chain_len(x.p, 0) <= 64 &&
+         chain_len(y.p, 0) <= 64 && R >= 16 / EG;
+}
+
+TmaPlan* tma_plan_create(const DirDev& x, const DirDev& y, const Layout& L, double* const arrays[3], int enable) {
+  TmaPlan* T = new TmaPlan();
+  if (!enable || !L.emaj || !encode_fn() || !tma_shape_ok(x, y)) return T;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&T->sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t ld8 = (uint64_t)L.ld * 8, Q8 = (uint64_t)L.Q * 8;
+  bool ok = true;
+  // ---- x-solve views: (column, e_x, kh) per x-parity; hat view = same with a narrow box
+  T->EG0 = NT / L.Q < 1 ? 1 : NT / L.Q;
+  if (T->EG0 > y.n) T->EG0 = y.n;
+  T->hw = even_up(T->EG0 + 2);
+  const int BW = T->EG0 * L.Q;
+  for (int a = 0; ok && a < 3; ++a) {
+    for (int pi = 0; ok && pi < 2; ++pi) {
+      const int mpi = chain_len(x.p, pi) > 0 ? chain_len(x.p, pi) : 1;
+      double* base = arrays[a] + (size_t)(x.nh + pi * x.n) * L.ld;
+      const uint64_t d[3] = {(uint64_t)L.ld, (uint64_t)x.n, (uint64_t)mpi};
+      const uint64_t s[2] = {ld8, 2 * (uint64_t)x.n * ld8};
+      const uint32_t b[3] = {(uint32_t)BW, 1, (uint32_t)KR};
+      ok = encode(&T->xv[a][pi], 3, base, d, s, b);
+    }
+    for (int pi = 0; ok && pi < 2; ++pi) {
+      // same geometry, narrow box over the hat columns h0 .. h0+hw-1
+      const int mpi = chain_len(x.p, pi) > 0 ? chain_len(x.p, pi) : 1;
+      double* base = arrays[a] + (size_t)(x.nh + pi * x.n) * L.ld;
+      const uint64_t d[3] = {(uint64_t)L.ld, (uint64_t)x.n, (uint64_t)mpi};
+      const uint64_t s[2] = {ld8, 2 * (uint64_t)x.n * ld8};
+      const uint32_t b[3] = {(uint32_t)T->hw, 1, (uint32_t)KR};
+      ok = encode(&T->xv[a][2 + pi], 3, base, d, s, b);
+    }
+  }
+  // ---- y-solve views
+  {
+    int EG, R;
+    y_tile_shape(x, y, EG, R);
+    const int RW = 16 / EG;
+    T->EG1 = EG;
+    T->R = R;
+    ok = ok && R >= RW;
+    for (int a = 0; ok && a < 3; ++a) {
+      for (int pi = 0; ok && pi < 2; ++pi) {
+        const int mpi = chain_len(x.p, pi);
+        double* base = arrays[a] + L.hb + (size_t)(x.nh + pi * x.n) * L.ld;
+        const uint64_t d4[4] = {(uint64_t)L.Q, (uint64_t)y.n, (uint64_t)x.n, (uint64_t)mpi};
+        const uint64_t s4[3] = {Q8, ld8, 2 * (uint64_t)x.n * ld8};
+        const uint32_t bG[4] = {KBOX, (uint32_t)EG, 1, (uint32_t)R};
+        const uint32_t bW[4] = {KBOX, (uint32_t)EG, 1, (uint32_t)R + 2};
+        ok = encode(&T->yG[a][pi], 4, base, d4, s4, bG) && encode(&T->yW[a][pi], 4, base, d4, s4, bW);
+        if (ok && a == 1) {
+          const uint32_t bO[4] = {16, (uint32_t)EG, 1, (uint32_t)RW};
+          ok = encode(&T->yO[pi], 4, base, d4, s4, bO);
+        }
+      }
+      if (ok) {
+        const uint64_t d3[3] = {(uint64_t)L.Q, (uint64_t)y.n, (uint64_t)x.N};
+        const uint64_t s3[2] = {Q8, ld8};
+        const uint32_t b3[3] = {KBOX, (uint32_t)EG, 2};
+        ok = encode(&T->yH[a], 3, arrays[a] + L.hb, d3, s3, b3);
+      }
+    }
+  }
+  T->ok = ok;
+  return T;
+}
+
+void tma_plan_destroy(TmaPlan* T) { delete T; }
+
+bool tma_supports(const TmaPlan* T, int dir) { return T && T->ok && (dir == 0 || dir == 1); }
+
+/* The dynamic shared-memory opt-in is set once per kernel instantiation:
+ * cudaFuncSetAttribute can serialise with in-flight launches of the same
+ * kernel, which would stall the host between half-steps. */
+constexpr int SMEM_OPTIN = 200 * 1024;
+
+template <typename K>
+static cudaError_t optin(K k, bool& done) {
+  if (done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_OPTIN);
+  if (e == cudaSuccess) done = true;
+  return e;
+}
+
+template <int CL, int MODE>
+static cudaError_t launch_x(const TmaStepArgs& A, const CUtensorMap* g, const CUtensorMap* w, int grid, size_t smem,
+                            cudaStream_t st) {
+  auto k = k_xstep_tma<CL, MODE>;
+  static bool done = false;
+  cudaError_t e = optin(k, done);
+  if (e != cudaSuccess) return e;
+  k<<<grid, NT, smem, st>>>(A, g[0], g[1], w[0], w[1], w[2], w[3]);
+  return cudaGetLastError();
+}
+
+template <int CL, int MODE>
+static cudaError_t launch_y(const TmaStepArgs& A, const TmaPlan* T, int gi, int wi, int grid, size_t smem,
+                            cudaStream_t st) {
+  auto k = k_ystep_tma<CL, MODE>;
+  static bool done = false;
+  cudaError_t e = optin(k, done);
+  if (e != cudaSuccess) return e;
+  k<<<grid, NT, smem, st>>>(A, T->yG[gi][0], T->yG[gi][1], T->yW[wi][0], T->yW[wi][1], T->yH[wi], T->yO[0],
+                            T->yO[1]);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t dispatch_x(int cl, const TmaStepArgs& A, const CUtensorMap* g, const CUtensorMap* w, int grid,
+                              size_t smem, cudaStream_t st) {
+  if (cl <= 8) return launch_x<8, MODE>(A, g, w, grid, smem, st);
+  if (cl <= 16) return launch_x<16, MODE>(A, g, w, grid, smem, st);
+  if (cl <= 32) return launch_x<32, MODE>(A, g, w, grid, smem, st);
+  return launch_x<64, MODE>(A, g, w, grid, smem, st);
+}
+
+template <int MODE>
+static cudaError_t dispatch_y(int cl, const TmaStepArgs& A, const TmaPlan* T, int gi, int wi, int grid, size_t smem,
+                              cudaStream_t st) {
+  if (cl <= 8) return launch_y<8, MODE>(A, T, gi, wi, grid, smem, st);
+  if (cl <= 16) return launch_y<16, MODE>(A, T, gi, wi, grid, smem, st);
+  if (cl <= 32) return launch_y<32, MODE>(A, T, gi, wi, grid, smem, st);
+  return launch_y<64, MODE>(A, T, gi, wi, grid, smem, st);
+}
+
+static int round128(int b) { return (b + 127) & ~127; }
+
+/* Launch the bubble-line part of one half-step.  ia_g / ia_w: indices of the
+ * G and Xp arrays among (Gp, X1, X2) (-1 when unused). */
+cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int ia_w, cudaStream_t st) {
+  TmaStepArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.P = P;
+  const int gi = ia_g >= 0 ? ia_g : ia_w, wi = ia_w >= 0 ? ia_w : ia_g;
+  const int budget = SMEM_OPTIN - 4096;
+  if (P.dir == 0) {
+    const DirDev& x = P.s;
+    const DirDev& y = P.o;
+    A.EG = T->EG0;
+    A.hw = T->hw;
+    const int BW = A.EG * P.lay.Q;
+    const int gb = (P.mode != ST_CORR) ? KR * BW * 8 : 0;
+    const int wb = (P.mode != ST_NONE) ? KR * BW * 8 : 0;
+    const int hb = (P.mode != ST_NONE) ? KR * A.hw * 8 : 0;
+    A.off_w = round128(gb);
+    A.off_h = A.off_w + round128(wb);
+    A.stage_bytes = round128(A.off_h + hb);
+    A.tx_bytes = gb + wb + hb;
+    A.fac_doubles = (P.f.cfs + 15) & ~15;
+    A.nstages = (budget - 2 * A.fac_doubles * 8) / A.stage_bytes;
+    if (A.nstages > 32) A.nstages = 32;
+    // the producer (thread 0, also a consumer) must never reach the tile after
+    // next: it would wait on a factor buffer its own warp has not released
+    {
+      int mins = (chain_len(x.p, 0) - 1) / KR + 1;
+      if (chain_len(x.p, 1) > 0) {
+        const int s1 = (chain_len(x.p, 1) - 1) / KR + 1;
+        if (s1 < mins) mins = s1;
+      }
+      if (A.nstages > mins) A.nstages = mins;
+    }
+    if (A.nstages < 1) A.nstages = 1;
+    A.fac_off = A.nstages * A.stage_bytes;
+    A.ntiles = ((y.n + A.EG - 1) / A.EG) * x.n * 2;
+    const size_t smem = (size_t)A.fac_off + 2 * A.fac_doubles * 8 + (2 * A.nstages + 2) * sizeof(uint64_t);
+    const int grid = A.ntiles < T->sms ? A.ntiles : T->sms;
+    const int cl = chain_len(x.p, 0);
+    const CUtensorMap* g = T->xv[gi];
+    const CUtensorMap* w = T->xv[wi];
+    switch (P.mode) {
+      case ST_NONE: return dispatch_x<ST_NONE>(cl, A, g, w, grid, smem, st);
+      case ST_APPLY: return dispatch_x<ST_APPLY>(cl, A, g, w, grid, smem, st);
+      default: return dispatch_x<ST_CORR>(cl, A, g, w, grid, smem, st);
+    }
+  }
+  const DirDev& y = P.s;
+  const DirDev& x = P.o;
+  A.EG = T->EG1;
+  A.R = T->R;
+  const int gb = (P.mode != ST_CORR) ? A.R * A.EG * KBOX * 8 : 0;
+  const int wb = (P.mode != ST_NONE) ? (A.R + 2) * A.EG * KBOX * 8 : 0;
+  const int hb = (P.mode != ST_NONE) ? 2 * A.EG * KBOX * 8 : 0;
+  A.off_w = round128(gb);
+  A.off_h = A.off_w + round128(wb);
+  A.stage_bytes = round128(A.off_h + hb);
+  A.tx_bytes = gb + wb + hb;
+  const int obytes = 2 * NW * 256 * 8;
+  A.fac_doubles = (2 * A.EG * P.f.cfs + 15) & ~15;
+  A.nstages = (budget - obytes - 2 * A.fac_doubles * 8) / A.stage_bytes;
+  if (A.nstages > 32) A.nstages = 32;
+  if (A.nstages > (chain_len(y.p, 0) - 1) / KCP + 1) A.nstages = (chain_len(y.p, 0) - 1) / KCP + 1;  // see x-solve
+  if (A.nstages < 1) A.nstages = 1;
+  A.out_off = A.nstages * A.stage_bytes;
+  A.fac_off = A.out_off + obytes;
+  const int nw = (chain_len(x.p, 0) + A.R - 1) / A.R + (chain_len(x.p, 1) + A.R - 1) / A.R;
+  A.ntiles = ((y.n + A.EG - 1) / A.EG) * x.n * nw;
+  const size_t smem = (size_t)A.fac_off + 2 * A.fac_doubles * 8 + (2 * A.nstages + 2) * sizeof(uint64_t);
+  const int grid = A.ntiles < T->sms ? A.ntiles : T->sms;
+  const int cl = chain_len(y.p, 0);
+  switch (P.mode) {
+    case ST_NONE: return dispatch_y<ST_NONE>(cl, A, T, gi, wi, grid, smem, st);
+    case ST_APPLY: return dispatch_y<ST_APPLY>(cl, A, T, gi, wi, grid, smem, st);
+    default: return dispatch_y<ST_CORR>(cl, A, T, gi, wi, grid, smem, st);
+  }
+}
+
+}  // namespace hpfem

@@ -1,0 +1,29 @@
+/*
+ * tma_step.h -- TMA-fed half-step kernels (tma_step.cu): tensor maps over
+ * the plan's internal arrays and the launcher for the bubble lines.
+ */
+#ifndef HPFEM_TMA_STEP_H_
+#define HPFEM_TMA_STEP_H_
+
+#include <cuda_runtime.h>
+
+#include "hpfem_internal.h"
+
+namespace hpfem {
+
+struct TmaPlan;
+
+/* shape conditions of the TMA path (it then needs the element-major layout) */
+bool tma_shape_ok(const DirDev& x, const DirDev& y);
+
+/* arrays = {Gp, X1, X2} (internal layout L); enable = 0 disables the path */
+TmaPlan* tma_plan_create(const DirDev& x, const DirDev& y, const Layout& L, double* const arrays[3], int enable);
+void tma_plan_destroy(TmaPlan* T);
+/* can the TMA kernel handle the bubble lines of a solve along dir? */
+bool tma_supports(const TmaPlan* T, int dir);
+/* bubble lines of one half-step; ia_g / ia_w index {Gp, X1, X2} (-1 = unused) */
+cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int ia_w, cudaStream_t st);
+
+}  // namespace hpfem
+
+#endif

@@ -42,8 +42,19 @@ SMALL = [
 ]
 
 
+@pytest.fixture(params=["tma", "ldg"])
+def kernel_path(request, monkeypatch):
+    """Run with the TMA half-step kernels (default) and with the LDG kernels
+    (HPFEM_NO_TMA=1, also the fallback for shapes TMA cannot express)."""
+    if request.param == "ldg":
+        monkeypatch.setenv("HPFEM_NO_TMA", "1")
+    else:
+        monkeypatch.delenv("HPFEM_NO_TMA", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("case", range(len(SMALL)))
-def test_small_cases(case):
+def test_small_cases(case, kernel_path):
     xs, px, ys, py, om, bc, tol = SMALL[case]
     plan = gpu_plan(xs, px, ys, py, om, bc, tol)
     ref = oracle.plan(xs, px, ys, py, om, bc, tol)
@@ -55,7 +66,7 @@ def test_small_cases(case):
     U = gpu_solve(plan, G)
     Uref, J = oracle.adi_solve(xs, px, ys, py, om, bc, tol, G)
     l2, plain = parity(xs, px, ys, py, bc, U, Uref)
-    print(f"case {case}: N={plan.Nx}x{plan.Ny} J={J} L2 {l2:.2e} plain {plain:.2e}")
+    print(f"case {case} [{kernel_path}]: N={plan.Nx}x{plan.Ny} J={J} L2 {l2:.2e} plain {plain:.2e}")
     assert l2 <= L2_TOL
 
 
@@ -122,7 +133,7 @@ def test_config_apply(i):
 
 
 @pytest.mark.parametrize("i", [1, 2, 3, 4])
-def test_config_full_solve(i):
+def test_config_full_solve(i, kernel_path):
     """Full ADI solve (all J iterations) vs the oracle at full size."""
     c, xs, ys, Fleg = _config_inputs(i)
     plan = gpu_plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
@@ -131,7 +142,7 @@ def test_config_full_solve(i):
     Uref, J = oracle.adi_solve(xs, c.px, ys, c.py, c.omega, c.bc, c.tol, G)
     assert J == plan.J
     l2, plain = parity(xs, c.px, ys, c.py, c.bc, U, Uref)
-    print(f"config {i}: J={J} L2 {l2:.3e} plain {plain:.3e}")
+    print(f"config {i} [{kernel_path}]: J={J} L2 {l2:.3e} plain {plain:.3e}")
     assert l2 <= L2_TOL
 
 
