@@ -28,13 +28,17 @@ struct DirDev {
  *   vL[b], vR[b] : D_e^{-1} B^T e_{hL(e)}, D_e^{-1} B^T e_{hR(e)} (static condensation)
  *   ilh[t], gh[t]: reverse Cholesky of the hat Schur complement A0 - B D^{-1} B^T
  *   cf           : chain-major copy for the TMA kernels, chain (e, pi) at
- *                  cf + (2e + pi) * cfs, position c at [3c] = il_c,
- *                  [3c+1] = g_c il_c, [3c+2] = g_{c-1} il_c, so that each
- *                  recurrence step is one dependent FMA:
- *                    y_c = il_c r_c - (g_c il_c) y_{c+1},
- *                    z_c = il_c y_c - (g_{c-1} il_c) z_{c-1};
- *                  cfs = 3 chain_len(p, 0) rounded up to even, + 2 (spreads
- *                  smem banks); one contiguous block per tile.
+ *                  cf + (2e + pi) * cfs, position c at
+ *                    [4c] = il_c, [4c+1] = hd_c = g_c il_c, [4c+2] = hu_c = g_{c-1} il_c,
+ *                  so that each recurrence step is one dependent FMA,
+ *                    y_c = il_c r_c - hd_c y_{c+1},   z_c = il_c y_c - hu_c z_{c-1},
+ *                  and [4c+3] = the spike coefficient of the two-thread split
+ *                  of the chain at M = ceil(chain_len(p,0)/2) (tma_step.cu):
+ *                    sigma_c (c < M): y_c = y^_c + sigma_c y_M,
+ *                      sigma_{M-1} = -hd_{M-1}, sigma_c = -hd_c sigma_{c+1};
+ *                    tau_c (c >= M):  z_c = z^_c + tau_c z_{M-1},
+ *                      tau_M = -hu_M, tau_c = -hu_c tau_{c-1};
+ *                  cfs = 4 chain_len(p, 0) + 2 (spreads smem banks).
  * stored contiguously: [il | g | vL | vR | ilh | gh | cf], 256-byte aligned. */
 struct FacView {
   const double* il;
@@ -48,7 +52,8 @@ struct FacView {
   double kap, sig;
 };
 
-HD int fac_cfs(const DirDev& d) { return ((3 * (d.p / 2) + 1) & ~1) + 2; }
+HD int fac_cfs(const DirDev& d) { return 4 * (d.p / 2) + 2; }
+HD int chain_split(int p) { return (((p / 2 + 1) / 2) + 3) & ~3; }  // multiple of 4 (TMA stage height)
 
 HD size_t fac_cf_off(const DirDev& d) {
   size_t s = 4 * (size_t)d.nb + 2 * (size_t)d.nh;

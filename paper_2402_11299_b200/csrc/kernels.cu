@@ -77,15 +77,26 @@ __global__ void k_factor_chains(DirDev d, const double* __restrict__ kap, const 
     g[b] = gc;
     lnext = l;
   }
-  {  // chain-major (il, g il, g_prev il) for the TMA kernels
+  {  // chain-major (il, g il, g_prev il, spike) for the TMA kernels (hpfem_internal.h)
     double* cf = base + fac_cf_off(d) + (size_t)(2 * e + pi) * fac_cfs(d);
     double gprev = 0.0;
     for (int c = 0; c < m; ++c) {
       const int b = (pi + 2 * c) * d.n + e;
-      cf[3 * c] = il[b];
-      cf[3 * c + 1] = g[b] * il[b];
-      cf[3 * c + 2] = gprev * il[b];
+      cf[4 * c] = il[b];
+      cf[4 * c + 1] = g[b] * il[b];
+      cf[4 * c + 2] = gprev * il[b];
       gprev = g[b];
+    }
+    const int M = chain_split(d.p);
+    double sgm = 1.0;
+    for (int c = (M < m ? M : m) - 1; c >= 0; --c) {  // sigma, bottom part
+      sgm = -cf[4 * c + 1] * sgm;
+      cf[4 * c + 3] = sgm;
+    }
+    double tau = 1.0;
+    for (int c = M; c < m; ++c) {  // tau, top part
+      tau = -cf[4 * c + 2] * tau;
+      cf[4 * c + 3] = tau;
     }
   }
   // v_side = T^{-1} (beta e_0): the chain-first bubble is the only one
@@ -262,6 +273,23 @@ __host__ __device__ __forceinline__ int ycol(const Layout& L, const DirDev& y, i
   if (d < y.nh) return d;
   const int b = d - y.nh, k = b / y.n;
   return ycol_ke(L, k, b - k * y.n);
+}
+
+/* y-dof stored at internal column li, -1 for padding columns */
+__device__ __forceinline__ int ydof_of_col(const Layout& L, const DirDev& y, int li) {
+  if (li < y.nh) return li;
+  if (li < L.hb) return -1;
+  const int b = li - L.hb;
+  int k, e;
+  if (L.emaj) {
+    e = b / L.Q;
+    k = b - e * L.Q;
+  } else {
+    k = b / L.np;
+    e = b - k * L.np;
+  }
+  if (e >= y.n || k >= y.p - 1) return -1;
+  return y.nh + k * y.n + e;
 }
 
 /* Address of (line l, dof position d) for a solve along DIR, both already in
@@ -468,13 +496,13 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
     return rh;
   };
   if (DIR == 0) {
-    // lines = columns: lane -> column (coalesced), thread groups over t
+    // lines = columns, taken in internal-column order: lane -> column (coalesced)
     const int j = threadIdx.x % LB, tg = threadIdx.x / LB, ng = blockDim.x / LB;
-    const int l = l0 + j;
-    if (l < P.o.N) {
+    const int li = l0 + j;
+    const int l = li < ld ? ydof_of_col(P.lay, P.o, li) : -1;
+    if (l >= 0) {
       Stencil st;
       line_stencil<DIR>(P, l, st);
-      const int li = ycol(P.lay, P.o, l);
       for (int t = tg; t < nh; t += ng) sh[t * LB + j] = rhs_hat(st, li, t);
     }
   } else {
@@ -491,7 +519,9 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
   }
   __syncthreads();
   // sequential tridiagonal reverse-Cholesky solve per line, in shared memory
-  if (threadIdx.x < LB && l0 + (int)threadIdx.x < P.o.N) {
+  const int nlines = DIR == 0 ? ld : P.o.N;
+  if (threadIdx.x < LB && l0 + (int)threadIdx.x < nlines &&
+      (DIR == 1 || ydof_of_col(P.lay, P.o, l0 + (int)threadIdx.x) >= 0)) {
     const int j = threadIdx.x;
     const double* __restrict__ ilh = P.f.ilh;
     const double* __restrict__ gh = P.f.gh;
@@ -510,11 +540,9 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
   __syncthreads();
   if (DIR == 0) {
     const int j = threadIdx.x % LB, tg = threadIdx.x / LB, ng = blockDim.x / LB;
-    const int l = l0 + j;
-    if (l < P.o.N) {
-      const int li = ycol(P.lay, P.o, l);
+    const int li = l0 + j;
+    if (li < ld && ydof_of_col(P.lay, P.o, li) >= 0)
       for (int t = tg; t < nh; t += ng) P.out[addr<DIR>(li, t, ld)] = sh[t * LB + j];
-    }
   } else {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int j = w; j < LB; j += nw) {
@@ -583,7 +611,8 @@ static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     opted = smem;
   }
-  k_hats<DIR, LB><<<(P.o.N + LB - 1) / LB, 256, smem, st>>>(P);
+  const int nlines = DIR == 0 ? P.ld : P.o.N;  // x-solve: internal columns (padding skipped)
+  k_hats<DIR, LB><<<(nlines + LB - 1) / LB, 256, smem, st>>>(P);
   return cudaGetLastError();
 }
 

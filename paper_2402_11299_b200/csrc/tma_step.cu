@@ -175,7 +175,8 @@ constexpr int KBOX = 18;   // y-solve: degrees per box row (16 + 2 to spread sme
 
 struct Producer {
   int tile, s;    // next stage to produce: tile and stage index within it (descending)
-  uint32_t it;    // its sequence number
+  int slot;       // its ring slot
+  uint32_t round; // how many times the ring has wrapped (phase of the slot's barriers)
   uint32_t tt;    // tiles started (selects the factor buffer)
   bool first;     // the next stage is the first of its tile
 };
@@ -200,8 +201,8 @@ __device__ __forceinline__ void x_produce(const TmaStepArgs& A, Producer& pr, un
   const int e_x = rest % x.n, pi = rest / x.n;
   const int col0 = P.lay.hb + g * EG * P.lay.Q;
   const int h0 = (y.bc == 0 ? g * EG - 1 : g * EG) & ~1;  // innermost TMA coordinate: 16-byte aligned
-  const int slot = pr.it % NST;
-  if (pr.it >= (uint32_t)NST) mbar_wait(&empty[slot], ((pr.it / NST) - 1) & 1);
+  const int slot = pr.slot;
+  if (pr.round >= 1) mbar_wait(&empty[slot], (pr.round - 1) & 1);
   unsigned char* st = ring + (size_t)slot * A.stage_bytes;
   if (pr.first) {  // the tile's chain factors ride with its first stage
     const uint32_t fb = pr.tt & 1;
@@ -219,7 +220,10 @@ __device__ __forceinline__ void x_produce(const TmaStepArgs& A, Producer& pr, un
     tma_load_3d(st + A.off_w, mW, &full[slot], col0, e_x, KR * pr.s);
     tma_load_3d(st + A.off_h, pi ? mH1 : mH0, &full[slot], h0, e_x, KR * pr.s);
   }
-  ++pr.it;
+  if (++pr.slot == NST) {
+    pr.slot = 0;
+    ++pr.round;
+  }
   pr.first = false;
   if (--pr.s < 0) {
     pr.tile += gridDim.x;
@@ -262,7 +266,8 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
   __syncthreads();
   if (threadIdx.x == 0) {
     pr.tile = blockIdx.x;
-    pr.it = 0;
+    pr.slot = 0;
+    pr.round = 0;
     pr.tt = 0;
     pr.first = true;
     pr.s = pr.tile < A.ntiles ? (chain_len(x.p, (pr.tile / ngroups) / x.n) - 1) / KR : -1;
@@ -270,13 +275,14 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
   }
   const int tid = threadIdx.x;
   const int eo = tid / Q, ky = tid - eo * Q;
-  uint32_t it = 0, ctt = 0;
+  int cslot = 0;
+  uint32_t cround = 0, ctt = 0;
   for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++ctt) {
     const int g = tile % ngroups, rest = tile / ngroups;
     const int e_x = rest % x.n, pi = rest / x.n;
     const int e0 = g * EG, ey = e0 + eo;
     const int m = chain_len(x.p, pi);
-    const double* fb = fbuf + (ctt & 1) * A.fac_doubles;  // [3c] il, [3c+1] g il, [3c+2] g_prev il
+    const double* fb = fbuf + (ctt & 1) * A.fac_doubles;  // [4c] il, [4c+1] g il, [4c+2] g_prev il
     const bool valid = eo < EG && ky < q && ey < y.n;
     const int h0 = (y.bc == 0 ? e0 - 1 : e0) & ~1;
     Sten5 st;
@@ -298,8 +304,8 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
 #pragma unroll
     for (int sg = CL / KR - 1; sg >= 0; --sg) {
       if (KR * sg < m) {
-        const int slot = it % NST;
-        mbar_wait(&full[slot], (it / NST) & 1);
+        const int slot = cslot;
+        mbar_wait(&full[slot], cround & 1);
         const unsigned char* stg = ring + (size_t)slot * A.stage_bytes;
         double rv[KR];
 #pragma unroll
@@ -315,13 +321,16 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
-        ++it;
+        if (++cslot == NST) {
+          cslot = 0;
+          ++cround;
+        }
         if (threadIdx.x == 0) x_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf, fempty);
 #pragma unroll
         for (int kk = KR - 1; kk >= 0; --kk) {
           const int c = KR * sg + kk;
           if (c < m) {
-            yv = fma(-fb[3 * c + 1], yv, fb[3 * c] * rv[kk]);
+            yv = fma(-fb[4 * c + 1], yv, fb[4 * c] * rv[kk]);
             ys[c] = yv;
           }
         }
@@ -333,7 +342,7 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
 #pragma unroll
       for (int c = 0; c < CL; ++c) {
         if (c < m) {
-          z = fma(-fb[3 * c + 2], z, fb[3 * c] * ys[c]);
+          z = fma(-fb[4 * c + 2], z, fb[4 * c] * ys[c]);
           out[(size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld] = z;
         }
       }
@@ -379,8 +388,8 @@ __device__ __forceinline__ void y_produce(const TmaStepArgs& A, Producer& pr, un
   const YTile t = y_decode(A, pr.tile);
   const int e0 = t.g * A.EG, kh0 = t.kw * A.R;
   const int hL = x.bc == 0 ? t.e_x - 1 : t.e_x;
-  const int slot = pr.it % NST;
-  if (pr.it >= (uint32_t)NST) mbar_wait(&empty[slot], ((pr.it / NST) - 1) & 1);
+  const int slot = pr.slot;
+  if (pr.round >= 1) mbar_wait(&empty[slot], (pr.round - 1) & 1);
   unsigned char* st = ring + (size_t)slot * A.stage_bytes;
   if (pr.first) {  // chain factors of the tile's EG elements x 2 parities (one contiguous block)
     const uint32_t fb = pr.tt & 1;
@@ -398,7 +407,10 @@ __device__ __forceinline__ void y_produce(const TmaStepArgs& A, Producer& pr, un
     tma_load_4d(st + A.off_w, t.pi ? mW1 : mW0, &full[slot], k0, e0, t.e_x, kh0 - 1);
     tma_load_3d(st + A.off_h, mH, &full[slot], k0, e0, hL);
   }
-  ++pr.it;
+  if (++pr.slot == NST) {
+    pr.slot = 0;
+    ++pr.round;
+  }
   pr.first = false;
   if (--pr.s < 0) {
     pr.tile += gridDim.x;
@@ -442,7 +454,8 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   if (threadIdx.x == 0) {
     pr.tile = blockIdx.x;
-    pr.it = 0;
+    pr.slot = 0;
+    pr.round = 0;
     pr.tt = 0;
     pr.first = true;
     pr.s = nst_tile - 1;
@@ -452,7 +465,8 @@ __global__ void __launch_bounds__(NT, 1)
   const int tid = threadIdx.x;
   const int eo = tid % EG, py = (tid / EG) & 1, r = tid / (2 * EG);
   const int cfs = P.f.cfs;
-  uint32_t it = 0, ctt = 0;
+  int cslot = 0;
+  uint32_t cround = 0, ctt = 0;
   int ob = 0;  // output staging buffer parity
   for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++ctt) {
     const YTile t = y_decode(A, tile);
@@ -481,8 +495,8 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
     for (int sg = CL / KCP - 1; sg >= 0; --sg) {
       if (KCP * sg < my) {
-        const int slot = it % NST;
-        mbar_wait(&full[slot], (it / NST) & 1);
+        const int slot = cslot;
+        mbar_wait(&full[slot], cround & 1);
         const unsigned char* stg = ring + (size_t)slot * A.stage_bytes;
         const double* Gs = reinterpret_cast<const double*>(stg);
         const double* Ws = reinterpret_cast<const double*>(stg + A.off_w);
@@ -499,15 +513,17 @@ __global__ void __launch_bounds__(NT, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
-        ++it;
+        if (++cslot == NST) {
+          cslot = 0;
+          ++cround;
+        }
         if (threadIdx.x == 0) y_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH, fbuf, fempty);
 #pragma unroll
         for (int u = KCP - 1; u >= 0; --u) {
           const int c = KCP * sg + u;
-          if (c < mthr) {
-            yv = fma(-fb[3 * c + 1], yv, fb[3 * c] * rv[u]);
-            ys[c] = yv;
-          }
+          const double yn = fma(-fb[4 * c + 1], yv, fb[4 * c] * rv[u]);
+          yv = c < mthr ? yn : 0.0;  // positions past this parity's chain stay 0
+          ys[c] = yv;
         }
       }
     }
@@ -525,11 +541,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int u = 0; u < KCP; ++u) {
           const int c = KCP * sg + u;
-          double zv = 0.0;
-          if (valid && c < mthr) {
-            z = fma(-fb[3 * c + 2], z, fb[3 * c] * ys[c]);
-            zv = z;
-          }
+          const double zn = fma(-fb[4 * c + 2], z, fb[4 * c] * ys[c]);
+          const bool live = valid && c < mthr;
+          z = live ? zn : z;
+          const double zv = live ? zn : 0.0;
           o[((r - wr0) * EG + eo) * 16 + py + 2 * u] = zv;
         }
         fence_proxy_async();
