@@ -601,9 +601,8 @@ cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st) {
   return P.dir == 0 ? launch_bub_dir<0>(P, st) : launch_bub_dir<1>(P, st);
 }
 
-template <int DIR>
-static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
-  constexpr int LB = 32;
+template <int DIR, int LB>
+static cudaError_t launch_hats_lb(const StepParams& P, cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)P.s.nh * LB;
   static size_t opted = 48 * 1024;
   if (smem > opted) {
@@ -614,6 +613,17 @@ static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
   const int nlines = DIR == 0 ? P.ld : P.o.N;  // x-solve: internal columns (padding skipped)
   k_hats<DIR, LB><<<(nlines + LB - 1) / LB, 256, smem, st>>>(P);
   return cudaGetLastError();
+}
+
+/* lines per CTA of the hat kernel (tuning knob HPFEM_HAT_LB_X / _Y: 8 or 32) */
+template <int DIR>
+static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
+  static int lb = -1;
+  if (lb < 0) {
+    const char* v = getenv(DIR == 0 ? "HPFEM_HAT_LB_X" : "HPFEM_HAT_LB_Y");
+    lb = v && *v ? atoi(v) : (DIR == 0 ? 32 : 8);
+  }
+  return lb == 8 ? launch_hats_lb<DIR, 8>(P, st) : launch_hats_lb<DIR, 32>(P, st);
 }
 
 cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st) {

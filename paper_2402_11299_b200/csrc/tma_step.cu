@@ -613,13 +613,42 @@ static int even_up(int v) { return (v + 1) & ~1; }
 /* y-solve tile shape: EG y-elements (a power of two <= 8, so that a warp
  * holds whole rows: RW = 16/EG rows per warp) x R rows of an x-chain (a
  * multiple of RW, with the R+2-row W box inside each parity's row count) */
-static void y_tile_shape(const DirDev& x, const DirDev& y, int& EG, int& R) {
-  EG = 8;
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+static void y_tile_shape_eg(const DirDev& x, const DirDev& y, int eg, int& EG, int& R) {
+  EG = eg;
   while (EG > y.n) EG >>= 1;
   const int RW = 16 / EG;
   R = NT / (2 * EG);
   if (R > chain_len(x.p, 1) - 2) R = chain_len(x.p, 1) - 2;
   R -= R % RW;
+}
+
+/* choose EG in {4, 8}: fewest idle rows in the x-chain windows, then the
+ * larger window (W rows reused R/(R+2)); HPFEM_EG_Y overrides */
+static void y_tile_shape(const DirDev& x, const DirDev& y, int& EG, int& R) {
+  const int forced = env_int("HPFEM_EG_Y", 0);
+  if (forced) {
+    y_tile_shape_eg(x, y, forced, EG, R);
+    return;
+  }
+  double best = -1.0;
+  for (int eg : {4, 8}) {
+    int e, r;
+    y_tile_shape_eg(x, y, eg, e, r);
+    if (r < 16 / e) continue;
+    const int m0 = chain_len(x.p, 0), m1 = chain_len(x.p, 1);
+    const double eff = double(m0 + m1) / double(((m0 + r - 1) / r + (m1 + r - 1) / r) * r);
+    if (eff > best + 1e-9) {
+      best = eff;
+      EG = e;
+      R = r;
+    }
+  }
+  if (best < 0) y_tile_shape_eg(x, y, 8, EG, R);
 }
 
 /* shape conditions of the TMA path (both directions, element-major layout) */
@@ -791,6 +820,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
       }
       if (A.nstages > mins) A.nstages = mins;
     }
+    if (A.nstages > env_int("HPFEM_NST_X", 3)) A.nstages = env_int("HPFEM_NST_X", 3);  // 3 measured best
     if (A.nstages < 1) A.nstages = 1;
     A.fac_off = A.nstages * A.stage_bytes;
     A.ntiles = ((y.n + A.EG - 1) / A.EG) * x.n * 2;
@@ -821,6 +851,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
   A.nstages = (budget - obytes - 2 * A.fac_doubles * 8) / A.stage_bytes;
   if (A.nstages > 32) A.nstages = 32;
   if (A.nstages > (chain_len(y.p, 0) - 1) / KCP + 1) A.nstages = (chain_len(y.p, 0) - 1) / KCP + 1;  // see x-solve
+  if (A.nstages > env_int("HPFEM_NST_Y", 99)) A.nstages = env_int("HPFEM_NST_Y", 99);
   if (A.nstages < 1) A.nstages = 1;
   A.out_off = A.nstages * A.stage_bytes;
   A.fac_off = A.out_off + obytes;
