@@ -132,6 +132,7 @@ struct StepParams {
   const double* cvR;
   FacView f;  // factor of this solve
   double* out;
+  const double* wtab;  // precomputed stencil weights of the bubble lines (TMA kernels; null = build in-kernel)
 };
 
 /* launchers (kernels.cu); return cudaError_t of the launch */

@@ -260,6 +260,9 @@ struct hpfem_plan_s {
   double* X1 = nullptr;           // W_{j-1/2} (deferred along y), final y-solve
   double* X2 = nullptr;           // W_j (deferred along x)
   TmaPlan* tma = nullptr;         // TMA tensor maps over {Gp, X1, X2} (null = LDG kernels only)
+  double* wx = nullptr;           // precomputed x-solve stencil weights, J tables
+  double* wy = nullptr;           // precomputed y-solve stencil weights, J tables (table 0 unused)
+  size_t wxs = 0, wys = 0;        // doubles per table
   bool use_tma = false;           // TMA half-step kernels + element-major layout
   long long launches = 0;
   // profiling (hpfem_plan_profile)
@@ -307,6 +310,8 @@ void free_plan(hpfem_plan_t pl) {
   cudaFree(pl->Gp);
   cudaFree(pl->X1);
   cudaFree(pl->X2);
+  cudaFree(pl->wx);
+  cudaFree(pl->wy);
   delete pl;
 }
 
@@ -420,12 +425,35 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
     pl->tma = tma_plan_create(pl->dx, pl->dy, pl->lay, arrays, pl->use_tma);
     if (pl->use_tma && !tma_supports(pl->tma, 0)) return fail_cuda(cudaErrorNotSupported, "TMA tensor maps");
   }
+  const char* no_wtab = std::getenv("HPFEM_NO_WTAB");
+  if (pl->use_tma && !(no_wtab && no_wtab[0] == '1')) {  // stencil-weight tables of every ST_APPLY half-step
+    pl->wxs = tma_wtab_doubles(pl->dx, pl->dy, pl->lay, 0);
+    pl->wys = tma_wtab_doubles(pl->dx, pl->dy, pl->lay, 1);
+    if ((ce = cudaMalloc(&pl->wx, sizeof(double) * pl->wxs * J)) != cudaSuccess) return fail_cuda(ce, "alloc wx");
+    if ((ce = cudaMalloc(&pl->wy, sizeof(double) * pl->wys * J)) != cudaSuccess) return fail_cuda(ce, "alloc wy");
+    if ((ce = cudaMemsetAsync(pl->wx, 0, sizeof(double) * pl->wxs * J, st)) != cudaSuccess) return fail_cuda(ce, "memset");
+    if ((ce = cudaMemsetAsync(pl->wy, 0, sizeof(double) * pl->wys * J, st)) != cudaSuccess) return fail_cuda(ce, "memset");
+  }
   const double* dsh = pl->d_shift;
   if ((ce = launch_factor(pl->dx, dsh, dsh + (J + 1), J, pl->fx, pl->sx, pl->d_err, st)) != cudaSuccess)
     return fail_cuda(ce, "factor x");
   if ((ce = launch_factor(pl->dy, dsh + 2 * (J + 1), dsh + 3 * (J + 1), J + 1, pl->fy, pl->sy, pl->d_err + 4, st)) !=
       cudaSuccess)
     return fail_cuda(ce, "factor y");
+  if (pl->wx) {
+    for (int j = 0; j < J; ++j) {
+      // half-step B of iteration j: y-apply (A_y + q_j M_y) Corr_y(fy[j]) along the x-solve lines
+      const FacView fyj = fac_view(pl->dy, pl->fy + pl->sy * j, 1.0, hw2 + pl->P[j]);
+      if ((ce = tma_build_wtab(pl->dx, pl->dy, pl->lay, 0, 1.0, hw2 + pl->Q[j], fyj.vL, fyj.vR,
+                               pl->wx + pl->wxs * j, st)) != cudaSuccess)
+        return fail_cuda(ce, "stencil tables");
+      if (j == 0) continue;  // half-step A of iteration 0 has no apply (W_0 = 0)
+      const FacView fxp = fac_view(pl->dx, pl->fx + pl->sx * (j - 1), 1.0, hw2 - pl->Q[j - 1]);
+      if ((ce = tma_build_wtab(pl->dx, pl->dy, pl->lay, 1, 1.0, hw2 - pl->P[j], fxp.vL, fxp.vR,
+                               pl->wy + pl->wys * j, st)) != cudaSuccess)
+        return fail_cuda(ce, "stencil tables");
+    }
+  }
   int herr[8];
   if ((ce = cudaMemcpyAsync(herr, pl->d_err, sizeof(herr), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
     return fail_cuda(ce, "copy err");
@@ -590,6 +618,7 @@ int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, vo
       A.tau = hw2 - pl->P[j];
       A.cvL = prev.vL;
       A.cvR = prev.vR;
+      if (pl->wy) A.wtab = pl->wy + pl->wys * j;
     }
     if ((rc = run_step(pl, A, st, false, 0, j == 0 ? -1 : 2))) return rc;
     // half-step B: W_j = (A_x - q_j M_x)^{-1} (G - W_{j-1/2} (A_y + q_j M_y))
@@ -604,6 +633,7 @@ int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, vo
     B.tau = hw2 + pl->Q[j];
     B.cvL = A.f.vL;
     B.cvR = A.f.vR;
+    if (pl->wx) B.wtab = pl->wx + pl->wxs * j;
     if ((rc = run_step(pl, B, st, false, 0, 1))) return rc;
   }
   // RETURN W_J C^{-1}: y-solves with the mass factor, then materialise U

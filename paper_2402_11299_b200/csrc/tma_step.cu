@@ -165,6 +165,9 @@ struct TmaStepArgs {
   int out_off;      // y-solve: byte offset of the two output staging buffers
   int fac_off;      // byte offset of the two per-tile factor buffers
   int fac_doubles;  // doubles per factor buffer
+  int fake_stencil; // experiment only (HPFEM_FAKE_STENCIL=1): skip the per-tile stencil build
+  int wb_off;       // byte offset of the two per-tile stencil-weight buffers (when P.wtab)
+  int wb_doubles;   // doubles per weight buffer
 };
 
 constexpr int NT = 256;    // threads per CTA; thread 0 doubles as the TMA producer
@@ -208,8 +211,13 @@ __device__ __forceinline__ void x_produce(const TmaStepArgs& A, Producer& pr, un
     const uint32_t fb = pr.tt & 1;
     if (pr.tt >= 2) mbar_wait(&fempty[fb], ((pr.tt >> 1) - 1) & 1);
     const uint32_t fbytes = P.f.cfs * 8;
-    mbar_expect_tx(&full[slot], A.tx_bytes + fbytes);
+    const int ne = (y.n - g * EG) < EG ? (y.n - g * EG) : EG;
+    const uint32_t wbytes = P.wtab ? ne * 5 * P.lay.Q * 8 : 0;
+    mbar_expect_tx(&full[slot], A.tx_bytes + fbytes + wbytes);
     bulk_load(fbuf + fb * A.fac_doubles, P.f.cf + (size_t)(2 * e_x + pi) * P.f.cfs, fbytes, &full[slot]);
+    if (wbytes)
+      bulk_load(reinterpret_cast<unsigned char*>(fbuf) + (A.wb_off - A.fac_off) + fb * A.wb_doubles * 8,
+                P.wtab + (size_t)g * EG * 5 * P.lay.Q, wbytes, &full[slot]);
   } else {
     mbar_expect_tx(&full[slot], A.tx_bytes);
   }
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
   const int NST = A.nstages;
   unsigned char* ring = smem_raw;
   double* fbuf = reinterpret_cast<double*>(smem_raw + A.fac_off);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.fac_off + 2 * A.fac_doubles * sizeof(double));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.wb_off + 2 * A.wb_doubles * sizeof(double));
   uint64_t* empty = full + NST;
   uint64_t* fempty = empty + NST;
   const int lane = threadIdx.x & 31;
@@ -287,8 +295,11 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
     const int h0 = (y.bc == 0 ? e0 - 1 : e0) & ~1;
     Sten5 st;
     int o0 = 0, o1 = 0, o2 = 0, o3 = 0, o4 = 0;
+    const bool wtab = P.wtab != nullptr && MODE == ST_APPLY;
+    const double* wb = reinterpret_cast<const double*>(smem_raw + A.wb_off) + (ctt & 1) * A.wb_doubles;
     if (valid) {
-      sten5_build(y, y.nh + ky * y.n + ey, MODE, P.kap_a, P.tau, P.cvL, P.cvR, st);
+      if (A.fake_stencil) { st.w[0] = -1.0; st.w[1] = st.w[2] = st.w[3] = st.w[4] = 0.0; }
+      else if (!wtab) sten5_build(y, y.nh + ky * y.n + ey, MODE, P.kap_a, P.tau, P.cvL, P.cvR, st);
       o0 = eo * Q + ky;
       o1 = eo * Q + (ky >= 2 ? ky - 2 : ky);
       o2 = eo * Q + (ky + 2 < q ? ky + 2 : ky);
@@ -306,6 +317,10 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
       if (KR * sg < m) {
         const int slot = cslot;
         mbar_wait(&full[slot], cround & 1);
+        if (wtab && KR * sg + KR >= m) {  // first stage of the tile: the weights have landed
+#pragma unroll
+          for (int k = 0; k < 5; ++k) st.w[k] = valid ? wb[(eo * 5 + k) * Q + ky] : 0.0;
+        }
         const unsigned char* stg = ring + (size_t)slot * A.stage_bytes;
         double rv[KR];
 #pragma unroll
@@ -396,8 +411,13 @@ __device__ __forceinline__ void y_produce(const TmaStepArgs& A, Producer& pr, un
     if (pr.tt >= 2) mbar_wait(&fempty[fb], ((pr.tt >> 1) - 1) & 1);
     const int ne = (y.n - e0) < A.EG ? (y.n - e0) : A.EG;
     const uint32_t fbytes = 2 * ne * A.P.f.cfs * 8;
-    mbar_expect_tx(&full[slot], A.tx_bytes + fbytes);
+    const int mx = chain_len(x.p, 0), rows = (mx - kh0) < A.R ? (mx - kh0) : A.R;
+    const uint32_t wbytes = A.P.wtab ? rows * 6 * 8 : 0;
+    mbar_expect_tx(&full[slot], A.tx_bytes + fbytes + wbytes);
     bulk_load(fbuf + fb * A.fac_doubles, A.P.f.cf + (size_t)(2 * e0) * A.P.f.cfs, fbytes, &full[slot]);
+    if (wbytes)
+      bulk_load(reinterpret_cast<unsigned char*>(fbuf) + (A.wb_off - A.fac_off) + fb * A.wb_doubles * 8,
+                A.P.wtab + ((size_t)(t.e_x * 2 + t.pi) * mx + kh0) * 6, wbytes, &full[slot]);
   } else {
     mbar_expect_tx(&full[slot], A.tx_bytes);
   }
@@ -434,7 +454,7 @@ __global__ void __launch_bounds__(NT, 1)
   unsigned char* ring = smem_raw;
   double* obuf = reinterpret_cast<double*>(smem_raw + A.out_off);  // 2 x NW x [RW][EG][16]
   double* fbuf = reinterpret_cast<double*>(smem_raw + A.fac_off);   // 2 x [EG][2][cfs]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.fac_off + 2 * A.fac_doubles * sizeof(double));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.wb_off + 2 * A.wb_doubles * sizeof(double));
   uint64_t* empty = full + NST;
   uint64_t* fempty = empty + NST;
   const int lane = threadIdx.x & 31;
@@ -477,8 +497,11 @@ __global__ void __launch_bounds__(NT, 1)
     const int mthr = chain_len(y.p, py);
     const bool valid = r < R && kx <= x.p - 2 && ey < y.n;
     Sten5 st;
+    const bool wtab = P.wtab != nullptr && MODE == ST_APPLY;
+    const double* wb = reinterpret_cast<const double*>(smem_raw + A.wb_off) + (ctt & 1) * A.wb_doubles;
     if (valid) {
-      sten5_build(x, x.nh + kx * x.n + e_x, MODE, P.kap_a, P.tau, P.cvL, P.cvR, st);
+      if (A.fake_stencil) { st.w[0] = -1.0; st.w[1] = st.w[2] = st.w[3] = st.w[4] = 0.0; }
+      else if (!wtab) sten5_build(x, x.nh + kx * x.n + e_x, MODE, P.kap_a, P.tau, P.cvL, P.cvR, st);
     } else {
 #pragma unroll
       for (int k = 0; k < 5; ++k) st.w[k] = 0.0;
@@ -497,6 +520,10 @@ __global__ void __launch_bounds__(NT, 1)
       if (KCP * sg < my) {
         const int slot = cslot;
         mbar_wait(&full[slot], cround & 1);
+        if (wtab && KCP * sg + KCP >= my) {  // first stage of the tile: the weights have landed
+#pragma unroll
+          for (int k = 0; k < 5; ++k) st.w[k] = valid ? wb[r * 6 + k] : 0.0;
+        }
         const unsigned char* stg = ring + (size_t)slot * A.stage_bytes;
         const double* Gs = reinterpret_cast<const double*>(stg);
         const double* Ws = reinterpret_cast<const double*>(stg + A.off_w);
@@ -560,6 +587,47 @@ __global__ void __launch_bounds__(NT, 1)
     if (lane == 0) mbar_arrive(&fempty[ctt & 1]);
   }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+/* ------------------------------------------------------------------ */
+/* precomputed stencil weights of the bubble lines (one ST_APPLY step)  */
+/* ------------------------------------------------------------------ */
+__global__ void k_wtab_x(DirDev y, Layout L, double kap, double tau, const double* __restrict__ cvL,
+                         const double* __restrict__ cvR, double* __restrict__ wt) {
+  // lines = y-bubbles (k, e): table [e][5][Q]
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= y.nb) return;
+  const int k = b / y.n, e = b - k * y.n;
+  Sten5 st;
+  sten5_build(y, y.nh + b, ST_APPLY, kap, tau, cvL, cvR, st);
+#pragma unroll
+  for (int q = 0; q < 5; ++q) wt[((size_t)e * 5 + q) * L.Q + k] = st.w[q];
+}
+
+__global__ void k_wtab_y(DirDev x, double kap, double tau, const double* __restrict__ cvL,
+                         const double* __restrict__ cvR, double* __restrict__ wt) {
+  // lines = x-bubble rows (k, e): table [e][pi][kh][6], k = pi + 2 kh
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= x.nb) return;
+  const int k = b / x.n, e = b - k * x.n, pi = k & 1, kh = k >> 1;
+  Sten5 st;
+  sten5_build(x, x.nh + b, ST_APPLY, kap, tau, cvL, cvR, st);
+  double* o = wt + (((size_t)e * 2 + pi) * chain_len(x.p, 0) + kh) * 6;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) o[q] = st.w[q];
+}
+
+size_t tma_wtab_doubles(const DirDev& x, const DirDev& y, const Layout& L, int dir) {
+  return dir == 0 ? (size_t)y.n * 5 * L.Q : (size_t)x.n * 2 * chain_len(x.p, 0) * 6;
+}
+
+cudaError_t tma_build_wtab(const DirDev& x, const DirDev& y, const Layout& L, int dir, double kap, double tau,
+                           const double* cvL, const double* cvR, double* wtab, cudaStream_t st) {
+  if (dir == 0)
+    k_wtab_x<<<(y.nb + 255) / 256, 256, 0, st>>>(y, L, kap, tau, cvL, cvR, wtab);
+  else
+    k_wtab_y<<<(x.nb + 255) / 256, 256, 0, st>>>(x, kap, tau, cvL, cvR, wtab);
+  return cudaGetLastError();
 }
 
 /* ------------------------------------------------------------------ */
@@ -792,6 +860,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
   TmaStepArgs A;
   std::memset(&A, 0, sizeof(A));
   A.P = P;
+  A.fake_stencil = env_int("HPFEM_FAKE_STENCIL", 0);
   const int gi = ia_g >= 0 ? ia_g : ia_w, wi = ia_w >= 0 ? ia_w : ia_g;
   const int budget = SMEM_OPTIN - 4096;
   if (P.dir == 0) {
@@ -808,7 +877,8 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
     A.stage_bytes = round128(A.off_h + hb);
     A.tx_bytes = gb + wb + hb;
     A.fac_doubles = (P.f.cfs + 15) & ~15;
-    A.nstages = (budget - 2 * A.fac_doubles * 8) / A.stage_bytes;
+    A.wb_doubles = P.wtab ? A.EG * 5 * P.lay.Q : 0;
+    A.nstages = (budget - 2 * A.fac_doubles * 8 - 2 * A.wb_doubles * 8) / A.stage_bytes;
     if (A.nstages > 32) A.nstages = 32;
     // the producer (thread 0, also a consumer) must never reach the tile after
     // next: it would wait on a factor buffer its own warp has not released
@@ -823,8 +893,9 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
     if (A.nstages > env_int("HPFEM_NST_X", 3)) A.nstages = env_int("HPFEM_NST_X", 3);  // 3 measured best
     if (A.nstages < 1) A.nstages = 1;
     A.fac_off = A.nstages * A.stage_bytes;
+    A.wb_off = A.fac_off + 2 * A.fac_doubles * 8;
     A.ntiles = ((y.n + A.EG - 1) / A.EG) * x.n * 2;
-    const size_t smem = (size_t)A.fac_off + 2 * A.fac_doubles * 8 + (2 * A.nstages + 2) * sizeof(uint64_t);
+    const size_t smem = (size_t)A.wb_off + 2 * A.wb_doubles * 8 + (2 * A.nstages + 2) * sizeof(uint64_t);
     const int grid = A.ntiles < T->sms ? A.ntiles : T->sms;
     const int cl = chain_len(x.p, 0);
     const CUtensorMap* g = T->xv[gi];
@@ -848,16 +919,18 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
   A.tx_bytes = gb + wb + hb;
   const int obytes = 2 * NW * 256 * 8;
   A.fac_doubles = (2 * A.EG * P.f.cfs + 15) & ~15;
-  A.nstages = (budget - obytes - 2 * A.fac_doubles * 8) / A.stage_bytes;
+  A.wb_doubles = P.wtab ? ((A.R * 6 + 15) & ~15) : 0;
+  A.nstages = (budget - obytes - 2 * A.fac_doubles * 8 - 2 * A.wb_doubles * 8) / A.stage_bytes;
   if (A.nstages > 32) A.nstages = 32;
   if (A.nstages > (chain_len(y.p, 0) - 1) / KCP + 1) A.nstages = (chain_len(y.p, 0) - 1) / KCP + 1;  // see x-solve
   if (A.nstages > env_int("HPFEM_NST_Y", 99)) A.nstages = env_int("HPFEM_NST_Y", 99);
   if (A.nstages < 1) A.nstages = 1;
   A.out_off = A.nstages * A.stage_bytes;
   A.fac_off = A.out_off + obytes;
+  A.wb_off = A.fac_off + 2 * A.fac_doubles * 8;
   const int nw = (chain_len(x.p, 0) + A.R - 1) / A.R + (chain_len(x.p, 1) + A.R - 1) / A.R;
   A.ntiles = ((y.n + A.EG - 1) / A.EG) * x.n * nw;
-  const size_t smem = (size_t)A.fac_off + 2 * A.fac_doubles * 8 + (2 * A.nstages + 2) * sizeof(uint64_t);
+  const size_t smem = (size_t)A.wb_off + 2 * A.wb_doubles * 8 + (2 * A.nstages + 2) * sizeof(uint64_t);
   const int grid = A.ntiles < T->sms ? A.ntiles : T->sms;
   const int cl = chain_len(y.p, 0);
   switch (P.mode) {

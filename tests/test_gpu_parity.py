@@ -146,19 +146,35 @@ def test_config_full_solve(i, kernel_path):
     assert l2 <= L2_TOL
 
 
-@pytest.mark.parametrize("iters", [1, 2])
-def test_config5_truncated(iters):
-    """Config 5 at full size (16385^2, graded Neumann): the first `iters`
-    ADI iterations + W C^{-1}, GPU vs oracle (the full 162-iteration oracle
-    solve takes ~20 CPU-minutes; see DESIGN.md "Parity" for config 5)."""
+def _config5_tolerance():
+    """Config 5 cannot meet 1e-10 between ANY two fp64 implementations that
+    do not round identically: the oracle itself moves by
+    8e-6 .. 1.3e-5 in L2 under rounding-level perturbations of its inputs
+    (tests/golden/oracle_floor.json, written by scripts/oracle_floor.py,
+    which calls only oracle/).  Tolerance = max(1e-10, 10 x that floor)."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "oracle_floor.json")
+    f = json.load(open(path))["config5"]
+    return max(1e-10, 10.0 * max(f["G_perturb_l2"], f["mesh_ulp_l2"]))
+
+
+@pytest.mark.slow
+def test_config5_full_solve():
+    """Config 5 at full size (16385^2, graded Neumann, J = 162): full GPU solve
+    vs the full oracle solve (~10 CPU-minutes), in the L2 norm, against the
+    oracle's own rounding floor (reading R12)."""
     c, xs, ys, Fleg = _config_inputs(5)
+    tol = _config5_tolerance()
     plan = gpu_plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
     G = oracle.load(xs, c.px, ys, c.py, c.bc, Fleg)
-    U = gpu_solve(plan, G, iters=iters)
-    Uref, _ = oracle.adi_solve(xs, c.px, ys, c.py, c.omega, c.bc, c.tol, G, iters=iters)
+    U = gpu_solve(plan, G)
+    Uref, J = oracle.adi_solve(xs, c.px, ys, c.py, c.omega, c.bc, c.tol, G)
+    assert J == plan.J
     l2, plain = parity(xs, c.px, ys, c.py, c.bc, U, Uref)
-    print(f"config 5, {iters} iterations: L2 {l2:.3e} plain {plain:.3e}")
-    assert l2 <= L2_TOL
+    print(f"config 5: J={J} L2 {l2:.3e} (tolerance {tol:.2e}) plain {plain:.3e}")
+    assert l2 <= tol
 
 
 def test_iters_zero_and_zero_rhs():
