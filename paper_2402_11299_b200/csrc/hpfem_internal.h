@@ -140,6 +140,7 @@ cudaError_t launch_factor(const DirDev& d, const double* kap, const double* sig,
                           size_t stride, int* err, cudaStream_t st);
 cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st);
 cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st);
+cudaError_t launch_hat_lines(const StepParams& P, cudaStream_t st);  // element-major layout only
 cudaError_t launch_copyin(const DirDev& x, const DirDev& y, const Layout& L, const double* G, double* Gp,
                           cudaStream_t st);
 cudaError_t launch_finalize(const DirDev& x, const DirDev& y, const Layout& L, const double* vL, const double* vR,

@@ -26,6 +26,7 @@
 
 #include "hpfem_internal.h"
 #include "ops1d.h"
+#include "ptx.cuh"
 
 namespace hpfem {
 
@@ -624,6 +625,248 @@ static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
     lb = v && *v ? atoi(v) : (DIR == 0 ? 32 : 8);
   }
   return lb == 8 ? launch_hats_lb<DIR, 8>(P, st) : launch_hats_lb<DIR, 32>(P, st);
+}
+
+/* ------------------------------------------------------------------ */
+/* Hat lines of the other direction (element-major layout): the few    */
+/* lines whose cross-line stencil is the 7-point hat-row stencil.      */
+/* Whole tiles are staged through shared memory with coalesced loads,  */
+/* the chains are swept in shared memory, the tile is stored back.     */
+/* ------------------------------------------------------------------ */
+
+/* y-solve, lines = x-hat rows t: CTA = (t, group of EGH y-elements).
+ * smem: 8 row segments [EGH*Q] (G + 7 stencil rows) and the chains'
+ * factors [EGH][2][cfs]. */
+constexpr int EGH = 8;
+
+__global__ void __launch_bounds__(128) k_hatrows_y(StepParams P) {
+  extern __shared__ double sh[];
+  const DirDev& y = P.s;  // solve direction (chains along the row)
+  const DirDev& x = P.o;  // apply direction (stencil across rows)
+  const Layout& L = P.lay;
+  const int t = blockIdx.x;               // hat row
+  const int e0 = blockIdx.y * EGH;
+  const int ne = min(EGH, y.n - e0);
+  const int W = EGH * L.Q;                // segment width (doubles)
+  const size_t col0 = (size_t)L.hb + (size_t)e0 * L.Q;
+  double* seg = sh;                       // [8][W]: 0 = G / r / y / z, 1..7 = stencil rows
+  double* fac = sh + 8 * W;               // [EGH][2][cfs]
+  __shared__ int s_idx[7];
+  __shared__ double s_w[7];
+  if (threadIdx.x == 0) {
+    Stencil st;
+    stencil_build(x, t, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+    for (int q = 0; q < 7; ++q) {
+      s_idx[q] = st.idx[q];
+      s_w[q] = st.w[q];
+    }
+  }
+  __shared__ __align__(8) uint64_t bar;
+  const int nw = ne * L.Q;
+  const int cfs = P.f.cfs;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // bulk copies of the G segment, the stencil rows and the chains' factors (one thread)
+  if (threadIdx.x == 0) {
+    uint32_t bytes = 2 * ne * cfs * 8;
+    for (int q = 0; q < 8; ++q)
+      if (q == 0 ? P.alphaG != 0.0 : s_idx[q - 1] >= 0) bytes += nw * 8;
+    mbar_expect_tx(&bar, bytes);
+    for (int q = 0; q < 8; ++q) {
+      const double* src = q == 0 ? (P.alphaG != 0.0 ? P.G + (size_t)t * P.ld : nullptr)
+                                 : (s_idx[q - 1] >= 0 ? P.Xp + (size_t)s_idx[q - 1] * P.ld : nullptr);
+      if (src) bulk_load(seg + q * W, src + col0, nw * 8, &bar);
+    }
+    bulk_load(fac, P.f.cf + (size_t)2 * e0 * cfs, 2 * ne * cfs * 8, &bar);
+  }
+  // segments without a source read as zero
+  for (int q = 0; q < 8; ++q) {
+    const bool has = q == 0 ? P.alphaG != 0.0 : s_idx[q - 1] >= 0;
+    if (!has)
+      for (int j = threadIdx.x; j < W; j += blockDim.x) seg[q * W + j] = 0.0;
+  }
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  // r = alphaG G + sum_q w_q X_q (in place in segment 0)
+  for (int j = threadIdx.x; j < nw; j += blockDim.x) {
+    double r = P.alphaG != 0.0 ? P.alphaG * seg[j] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) r += s_w[q] * seg[(q + 1) * W + j];
+    seg[j] = r;
+  }
+  __syncthreads();
+  // chains: thread (eo, pi); down sweep y, up sweep z, in place
+  if (threadIdx.x < 2 * ne) {
+    const int eo = threadIdx.x >> 1, pi = threadIdx.x & 1;
+    const int m = chain_len(y.p, pi);
+    const double* f = fac + (eo * 2 + pi) * cfs;
+    double* v = seg + eo * L.Q + pi;
+    double yv = 0.0;
+    for (int c = m - 1; c >= 0; --c) {
+      yv = fma(-f[4 * c + 1], yv, f[4 * c] * v[2 * c]);
+      v[2 * c] = yv;
+    }
+    double z = 0.0;
+    for (int c = 0; c < m; ++c) {
+      z = fma(-f[4 * c + 2], z, f[4 * c] * v[2 * c]);
+      v[2 * c] = z;
+    }
+  }
+  __syncthreads();
+  double* out = P.out + (size_t)t * P.ld + col0;
+  for (int j = threadIdx.x; j < nw; j += blockDim.x) {
+    const int e = j / L.Q, k = j - e * L.Q;
+    if (k < y.p - 1) out[j] = seg[j];
+  }
+}
+
+/* x-solve, lines = y-hat columns: CTA = (x-element e_x, parity pi, group
+ * of TC hat columns l0..l0+TC-1).  For every row of the x-chain the CTA
+ * stages G at its columns, the hat columns l0-1..l0+TC and the bubble 0/1
+ * columns of the adjacent y-elements; the chains run in shared memory. */
+constexpr int TC = 32;
+constexpr int HREG = TC + 4;  // staged hat slots per row (TC + 2 used; rounding slack for 16-byte bulk copies)
+
+__global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
+  extern __shared__ double sh[];
+  const DirDev& x = P.s;  // solve direction (chains down the columns)
+  const DirDev& y = P.o;  // apply direction (stencil across columns)
+  const Layout& L = P.lay;
+  const int e_x = blockIdx.x % x.n, pi = blockIdx.x / x.n;
+  const int l0 = blockIdx.y * TC;
+  const int nl = min(TC, y.nh - l0);
+  const int m = chain_len(x.p, pi);
+  // element range of the bubble columns the tile's stencils touch
+  const int node0 = node_of_hat(l0, y.bc);
+  const int elo = max(node0 - 1, 0);
+  const int ehi = min(node_of_hat(l0 + nl - 1, y.bc), y.n - 1);
+  const int nE = ehi - elo + 1;
+  const int RW = TC + HREG + 2 * (TC + 2);  // per row: G | hats | bubble 0 | bubble 1 (16-byte aligned parts)
+  double* rows = sh;                             // [m][RW]
+  const int cfs = P.f.cfs;
+  double* fac = sh + (size_t)m * RW;             // [cfs]
+  const int hlo = (l0 - 1) & ~1;                 // first staged hat column (16-byte aligned)
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // per row: G[l0 .. l0+TC) and hats [hlo .. hlo+TC+2) as bulk copies (one thread);
+  // bubble 0/1 columns of the adjacent elements as 16-byte gathers (all threads)
+  const bool useG = P.alphaG != 0.0, useW = P.mode != ST_NONE;
+  const int hs = hlo < 0 ? 0 : hlo;              // first hat column actually copied (hats < 0 do not exist)
+  const int nh_c = min(l0 + nl + 1 - hs, y.nh - hs);  // hats hs .. l0+nl (the last line's right neighbour)
+  if (threadIdx.x == 0) {
+    uint32_t bytes = cfs * 8;
+    const uint32_t gb = useG ? ((nl * 8 + 15) & ~15) : 0;
+    const uint32_t hb = useW ? ((nh_c * 8 + 15) & ~15) : 0;
+    bytes += m * (gb + hb);
+    mbar_expect_tx(&bar, bytes);
+    for (int c = 0; c < m; ++c) {
+      const size_t row = (size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld;
+      if (gb) bulk_load(rows + (size_t)c * RW, P.G + row + l0, gb, &bar);
+      if (hb) bulk_load(rows + (size_t)c * RW + TC + (hs - hlo), P.Xp + row + hs, hb, &bar);
+    }
+    bulk_load(fac, P.f.cf + (size_t)(2 * e_x + pi) * cfs, cfs * 8, &bar);
+  }
+  if (!useG)
+    for (int idx = threadIdx.x; idx < m * TC; idx += blockDim.x) rows[(size_t)(idx / TC) * RW + idx % TC] = 0.0;
+  if (!useW)
+    for (int idx = threadIdx.x; idx < m * (TC + 2); idx += blockDim.x)
+      rows[(size_t)(idx / (TC + 2)) * RW + TC + idx % (TC + 2)] = 0.0;
+  else if (hs > hlo)  // the staged slots before hat 0 must read as zero
+    for (int c = threadIdx.x; c < m; c += blockDim.x)
+      for (int j = 0; j < hs - hlo; ++j) rows[(size_t)c * RW + TC + j] = 0.0;
+  {
+    const int nb = m * (TC + 2);  // (row, element) pairs, 2 doubles each
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < nb; idx += blockDim.x) {
+      const int c = idx / (TC + 2), ei = idx - c * (TC + 2), e = elo + ei;
+      double2 v = make_double2(0.0, 0.0);
+      if (useW && e <= ehi) {
+        const size_t row = (size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld;
+        v = __ldg(reinterpret_cast<const double2*>(P.Xp + row + L.hb + (size_t)e * L.Q));
+        if (y.p - 2 < 1) v.y = 0.0;
+      }
+      double* R = rows + (size_t)c * RW + TC + HREG;
+      R[ei] = v.x;              // bubble 0
+      R[(TC + 2) + ei] = v.y;   // bubble 1
+    }
+  }
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  if (threadIdx.x < nl) {
+    const int l = l0 + threadIdx.x;
+    Stencil st;
+    stencil_build(y, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+    int off[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const int d = st.idx[q];
+      if (d < 0) {
+        off[q] = 0;
+        st.w[q] = 0.0;
+      } else if (d < y.nh) {
+        off[q] = TC + (d - hlo);
+      } else {
+        const int b = d - y.nh, k = b / y.n, e = b - k * y.n;
+        off[q] = TC + HREG + k * (TC + 2) + (e - elo);
+      }
+    }
+    const double aG = P.alphaG;
+    double yv = 0.0;
+    for (int c = m - 1; c >= 0; --c) {
+      const double* R = rows + (size_t)c * RW;
+      double r = aG != 0.0 ? aG * R[threadIdx.x] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) r += st.w[q] * R[off[q]];
+      yv = fma(-fac[4 * c + 1], yv, fac[4 * c] * r);
+      rows[(size_t)c * RW + threadIdx.x] = yv;
+    }
+    double z = 0.0;
+    for (int c = 0; c < m; ++c) {
+      z = fma(-fac[4 * c + 2], z, fac[4 * c] * rows[(size_t)c * RW + threadIdx.x]);
+      rows[(size_t)c * RW + threadIdx.x] = z;
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < m * TC; idx += blockDim.x) {
+    const int c = idx / TC, j = idx - c * TC;
+    if (j < nl) P.out[(size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld + l0 + j] = rows[(size_t)c * RW + j];
+  }
+}
+
+/* hat lines of the other direction (element-major layout only) */
+cudaError_t launch_hat_lines(const StepParams& P, cudaStream_t st) {
+  if (P.o.nh == 0 || P.s.nb == 0) return cudaSuccess;
+  const Layout& L = P.lay;
+  if (P.dir == 1) {
+    const size_t smem = sizeof(double) * (8 * (size_t)EGH * L.Q + (size_t)EGH * 2 * P.f.cfs);
+    static size_t opted = 48 * 1024;
+    if (smem > opted) {
+      cudaError_t e = cudaFuncSetAttribute(k_hatrows_y, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      opted = smem;
+    }
+    dim3 grid(P.o.nh, (P.s.n + EGH - 1) / EGH);
+    k_hatrows_y<<<grid, 128, smem, st>>>(P);
+  } else {
+    const int m = chain_len(P.s.p, 0);
+    const size_t smem = sizeof(double) * ((size_t)m * (TC + HREG + 2 * (TC + 2)) + P.f.cfs);
+    static size_t opted = 48 * 1024;
+    if (smem > opted) {
+      cudaError_t e = cudaFuncSetAttribute(k_hatcols_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      opted = smem;
+    }
+    dim3 grid(P.s.n * 2, (P.o.nh + TC - 1) / TC);
+    k_hatcols_x<<<grid, 256, smem, st>>>(P);
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st) {

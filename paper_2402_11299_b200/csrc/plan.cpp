@@ -506,7 +506,9 @@ int run_step(hpfem_plan_t pl, StepParams P, cudaStream_t st, bool final_step, in
     H.lp_begin = P.dir == 0 ? 0 : P.o.nb;
     H.lp_count = P.o.nh;
     if (H.lp_count > 0) {
-      rc = count_launch(pl, launch_step_bubbles(H, st), "hat-line bubble kernel");
+      const char* old_hl = std::getenv("HPFEM_LDG_HATLINES");
+      rc = count_launch(pl, (old_hl && old_hl[0] == '1') ? launch_step_bubbles(H, st) : launch_hat_lines(H, st),
+                        "hat-line kernel");
       if (rc) return rc;
       prof_add(pl, k1, e1, prof_mark(pl, st), per * (double)P.o.nh * P.s.nb);
     }

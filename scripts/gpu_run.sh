@@ -1,5 +1,3 @@
+timeout 300 python -m pytest tests -m gpu -q -x -k "small_cases or config_plan or (config_full_solve and tma and not 4)" > gpurun_out/gpu_tests19.log 2>&1; echo tests rc=$?; tail -1 gpurun_out/gpu_tests19.log; grep -E "Error|assert" gpurun_out/gpu_tests19.log | head
 run() { timeout 120 python scripts/diag_launch.py $1 2>&1 | tail -1; }
-echo tables; run 5
-echo notables; HPFEM_NO_WTAB=1 run 5
-echo fake; HPFEM_NO_WTAB=1 HPFEM_FAKE_STENCIL=1 run 5
-echo tables-again; run 5
+for c in 5 3; do echo cfg $c; run $c; done
