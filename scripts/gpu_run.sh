@@ -1,3 +1,3 @@
-timeout 300 python -m pytest tests -m gpu -q -x -k "small_cases or config_plan or (config_full_solve and tma and not 4)" > gpurun_out/gpu_tests19.log 2>&1; echo tests rc=$?; tail -1 gpurun_out/gpu_tests19.log; grep -E "Error|assert" gpurun_out/gpu_tests19.log | head
-run() { timeout 120 python scripts/diag_launch.py $1 2>&1 | tail -1; }
-for c in 5 3; do echo cfg $c; run $c; done
+CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+$CMD > gpurun_out/plain.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"tma|hatrows|hatcols|k_hats" -s 12 -c 6 -o gpurun_out/prof6_c5 $CMD > gpurun_out/ncu9.log 2>&1; echo ncu rc=$?
+ncu --metrics gpu__time_duration.sum --clock-control none -s 2938 -c 978 --csv --log-file gpurun_out/launches_c5_v6.csv $CMD > gpurun_out/ncu10.log 2>&1; echo ncu2 rc=$?
