@@ -86,12 +86,28 @@ __device__ __forceinline__ void sten5_build(const DirDev& o, int l, int mode, do
   st.w[4] = hR ? -cR : 0.0;
 }
 
+/* n / d for 0 <= n < 2^31 by multiply-high (divisor fixed per launch) */
+struct FDiv {
+  uint32_t d, m, l;
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> l; }
+};
+
+static inline FDiv make_fdiv(uint32_t d) {
+  FDiv f;
+  f.d = d < 1 ? 1 : d;
+  f.l = 0;
+  while ((1u << f.l) < f.d) ++f.l;
+  f.m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << f.l) - f.d)) / f.d + 1);
+  return f;
+}
+
 struct TmaStepArgs {
   StepParams P;
   int EG;           // y-elements per tile
   int R;            // rows per tile (y-solve)
   int ntiles;
-  int nstages;
+  int nstages;      // ring depth NST (<= S, see below)
+  int S;            // stages per tile (the same for every tile of a launch)
   int stage_bytes;  // bytes per ring stage (all boxes, 128-aligned)
   int off_w, off_h; // byte offsets of the W and hat boxes inside a stage
   int tx_bytes;     // bytes the TMA delivers per stage
@@ -102,21 +118,38 @@ struct TmaStepArgs {
   int fake_stencil; // experiment only (HPFEM_FAKE_STENCIL=1): skip the per-tile stencil build
   int wb_off;       // byte offset of the two per-tile stencil-weight buffers (when P.wtab)
   int wb_doubles;   // doubles per weight buffer
+  int bar_off;      // byte offset of the full barriers [NST] and release counters [NST]
+  int nwt;          // y-solve: row windows per x-element (both parities)
+  FDiv fS, fN, fG, fT;  // divisions by S, NST, #element groups, and x.n (x-solve) / nwt (y-solve)
 };
 
-constexpr int NT = 256;    // threads per CTA; thread 0 doubles as the TMA producer
+constexpr int NT = 256;    // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int KR = 8;      // x-solve: chain positions (rows) per stage
 constexpr int KCP = 8;     // y-solve: chain positions per stage (16 degrees)
 constexpr int KBOX = 18;   // y-solve: degrees per box row (16 + 2 to spread smem banks)
 
-struct Producer {
-  int tile, s;    // next stage to produce: tile and stage index within it (descending)
-  int slot;       // its ring slot
-  uint32_t round; // how many times the ring has wrapped (phase of the slot's barriers)
-  uint32_t tt;    // tiles started (selects the factor buffer)
-  bool first;     // the next stage is the first of its tile
-};
+/* Ring discipline.  Every tile of a launch has the same number S of stages
+ * and this CTA's stages are numbered gs = 0, 1, ... in consumption order
+ * (tile-local index gs / S, stage S-1 - gs % S of it); stage gs lives in slot
+ * gs % NST and is complete when full[slot] flips.  There is no producer
+ * thread: each warp, after reading a stage, bumps the slot's release counter,
+ * and the warp that releases it LAST issues stage gs + NST into it (a handful
+ * of instructions: the coordinates are a pure function of gs).  No warp ever
+ * waits for another to release a slot.  A tile's chain factors (and stencil
+ * weights) ride with its first stage into buffer (tile-local index & 1);
+ * with NST <= S the first stage of tile t is issued only after every warp has
+ * read a stage of tile t-1, i.e. after every warp has finished tile t-2,
+ * the last user of that buffer. */
+__device__ __forceinline__ bool release_is_last(uint32_t* cnt, int slot) {
+  __threadfence_block();
+  const uint32_t old = atomicAdd(&cnt[slot], 1u);
+  if (old != NW - 1) return false;
+  cnt[slot] = 0;
+  __threadfence_block();
+  fence_proxy_async();
+  return true;
+}
 
 /* ------------------------------------------------------------------ */
 /* x-solve (DIR 0), element-major layout                               */
@@ -124,26 +157,27 @@ struct Producer {
 /* s = chain positions [KR s, KR s + KR) of the x-chain (rows)         */
 /* ------------------------------------------------------------------ */
 template <int MODE>
-__device__ __forceinline__ void x_produce(const TmaStepArgs& A, Producer& pr, unsigned char* ring, uint64_t* full,
-                                          uint64_t* empty, const CUtensorMap* mG0, const CUtensorMap* mG1,
-                                          const CUtensorMap* mW0, const CUtensorMap* mW1, const CUtensorMap* mH0,
-                                          const CUtensorMap* mH1, double* fbuf, uint64_t* fempty) {
+__device__ __forceinline__ void x_issue(const TmaStepArgs& A, uint32_t gs, unsigned char* ring, uint64_t* full,
+                                        const CUtensorMap* mG0, const CUtensorMap* mG1, const CUtensorMap* mW0,
+                                        const CUtensorMap* mW1, const CUtensorMap* mH0, const CUtensorMap* mH1,
+                                        double* fbuf) {
   const StepParams& P = A.P;
   const DirDev& x = P.s;
   const DirDev& y = P.o;
-  const int NST = A.nstages, EG = A.EG;
-  const int ngroups = (y.n + EG - 1) / EG;
-  if (pr.tile >= A.ntiles) return;
-  const int g = pr.tile % ngroups, rest = pr.tile / ngroups;
-  const int e_x = rest % x.n, pi = rest / x.n;
-  const int col0 = P.lay.hb + g * EG * P.lay.Q;
-  const int h0 = (y.bc == 0 ? g * EG - 1 : g * EG) & ~1;  // innermost TMA coordinate: 16-byte aligned
-  const int slot = pr.slot;
-  if (pr.round >= 1) mbar_wait(&empty[slot], (pr.round - 1) & 1);
+  const uint32_t tl = A.fS.div(gs);
+  const int s = A.S - 1 - (int)(gs - tl * A.S);
+  const int tile = blockIdx.x + (int)tl * gridDim.x;
+  if (tile >= A.ntiles) return;
+  const int slot = (int)(gs - A.fN.div(gs) * A.nstages);
+  const int rest = (int)A.fG.div(tile), g = tile - rest * (int)A.fG.d;
+  const int pi = (int)A.fT.div(rest), e_x = rest - pi * x.n;
+  const int EG = A.EG;
+  const int c0 = P.lay.hb + g * EG * P.lay.Q;
+  const int hc = (y.bc == 0 ? g * EG - 1 : g * EG) & ~1;  // innermost TMA coordinate: 16-byte aligned
+  const int row = KR * s < chain_len(x.p, pi) ? KR * s : 0;  // a stage past this parity's chain: any rows (unused)
   unsigned char* st = ring + (size_t)slot * A.stage_bytes;
-  if (pr.first) {  // the tile's chain factors ride with its first stage
-    const uint32_t fb = pr.tt & 1;
-    if (pr.tt >= 2) mbar_wait(&fempty[fb], ((pr.tt >> 1) - 1) & 1);
+  if (s == A.S - 1) {  // the tile's chain factors ride with its first stage
+    const uint32_t fb = tl & 1;
     const uint32_t fbytes = P.f.cfs * 8;
     const int ne = (y.n - g * EG) < EG ? (y.n - g * EG) : EG;
     const uint32_t wbytes = P.wtab ? ne * 5 * P.lay.Q * 8 : 0;
@@ -155,23 +189,10 @@ __device__ __forceinline__ void x_produce(const TmaStepArgs& A, Producer& pr, un
   } else {
     mbar_expect_tx(&full[slot], A.tx_bytes);
   }
-  const CUtensorMap* mG = pi ? mG1 : mG0;
-  const CUtensorMap* mW = pi ? mW1 : mW0;
-  if (MODE != ST_CORR) tma_load_3d(st, mG, &full[slot], col0, e_x, KR * pr.s);
+  if (MODE != ST_CORR) tma_load_3d(st, pi ? mG1 : mG0, &full[slot], c0, e_x, row);
   if (MODE != ST_NONE) {
-    tma_load_3d(st + A.off_w, mW, &full[slot], col0, e_x, KR * pr.s);
-    tma_load_3d(st + A.off_h, pi ? mH1 : mH0, &full[slot], h0, e_x, KR * pr.s);
-  }
-  if (++pr.slot == NST) {
-    pr.slot = 0;
-    ++pr.round;
-  }
-  pr.first = false;
-  if (--pr.s < 0) {
-    pr.tile += gridDim.x;
-    ++pr.tt;
-    pr.first = true;
-    if (pr.tile < A.ntiles) pr.s = (chain_len(x.p, (pr.tile / ngroups) / x.n) - 1) / KR;
+    tma_load_3d(st + A.off_w, pi ? mW1 : mW0, &full[slot], c0, e_x, row);
+    tma_load_3d(st + A.off_h, pi ? mH1 : mH0, &full[slot], hc, e_x, row);
   }
 }
 
@@ -189,36 +210,24 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
   const int NST = A.nstages;
   unsigned char* ring = smem_raw;
   double* fbuf = reinterpret_cast<double*>(smem_raw + A.fac_off);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.wb_off + 2 * A.wb_doubles * sizeof(double));
-  uint64_t* empty = full + NST;
-  uint64_t* fempty = empty + NST;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.bar_off);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(full + NST);
   const int lane = threadIdx.x & 31;
   const int EG = A.EG, q = y.p - 1, Q = P.lay.Q, BW = EG * Q;
   const int ngroups = (y.n + EG - 1) / EG;
-  Producer pr;
+  if (threadIdx.x < NST) cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
-    for (int k = 0; k < NST; ++k) {
-      mbar_init(&full[k], 1);
-      mbar_init(&empty[k], NW);
-    }
-    mbar_init(&fempty[0], NW);
-    mbar_init(&fempty[1], NW);
+    for (int k = 0; k < NST; ++k) mbar_init(&full[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    pr.tile = blockIdx.x;
-    pr.slot = 0;
-    pr.round = 0;
-    pr.tt = 0;
-    pr.first = true;
-    pr.s = pr.tile < A.ntiles ? (chain_len(x.p, (pr.tile / ngroups) / x.n) - 1) / KR : -1;
-    for (int k = 0; k < NST; ++k) x_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf, fempty);
-  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NST; ++k) x_issue<MODE>(A, k, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
   const int tid = threadIdx.x;
   const int eo = tid / Q, ky = tid - eo * Q;
+  const int mS = chain_len(x.p, 0);  // stages per tile cover the longer (even) chain
   int cslot = 0;
-  uint32_t cround = 0, ctt = 0;
+  uint32_t cround = 0, ctt = 0, gs = 0;
   for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++ctt) {
     const int g = tile % ngroups, rest = tile / ngroups;
     const int e_x = rest % x.n, pi = rest / x.n;
@@ -248,10 +257,10 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
     double yv = 0.0;
 #pragma unroll
     for (int sg = CL / KR - 1; sg >= 0; --sg) {
-      if (KR * sg < m) {
+      if (KR * sg < mS) {
         const int slot = cslot;
         mbar_wait(&full[slot], cround & 1);
-        if (wtab && KR * sg + KR >= m) {  // first stage of the tile: the weights have landed
+        if (wtab && KR * sg + KR >= mS) {  // first stage of the tile: the weights have landed
 #pragma unroll
           for (int k = 0; k < 5; ++k) st.w[k] = valid ? wb[(eo * 5 + k) * Q + ky] : 0.0;
         }
@@ -269,12 +278,13 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
           rv[kk] = r;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (lane == 0 && release_is_last(cnt, slot))
+          x_issue<MODE>(A, gs + NST, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
+        ++gs;
         if (++cslot == NST) {
           cslot = 0;
           ++cround;
         }
-        if (threadIdx.x == 0) x_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf, fempty);
 #pragma unroll
         for (int kk = KR - 1; kk >= 0; --kk) {
           const int c = KR * sg + kk;
@@ -296,8 +306,6 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&fempty[ctt & 1]);
   }
 }
 
@@ -311,38 +319,35 @@ struct YTile {
 };
 
 __device__ __forceinline__ YTile y_decode(const TmaStepArgs& A, int tile) {
-  const DirDev& y = A.P.s;
   const DirDev& x = A.P.o;
-  const int ngroups = (y.n + A.EG - 1) / A.EG;
-  const int nw0 = (chain_len(x.p, 0) + A.R - 1) / A.R, nw1 = (chain_len(x.p, 1) + A.R - 1) / A.R;
+  const int nw0 = (chain_len(x.p, 0) + A.R - 1) / A.R;
   YTile t;
-  t.g = tile % ngroups;
-  const int rest = tile / ngroups;
-  t.e_x = rest / (nw0 + nw1);
-  const int w = rest % (nw0 + nw1);
+  const int rest = (int)A.fG.div(tile);
+  t.g = tile - rest * (int)A.fG.d;
+  t.e_x = (int)A.fT.div(rest);
+  const int w = rest - t.e_x * A.nwt;
   t.pi = w < nw0 ? 0 : 1;
   t.kw = t.pi == 0 ? w : w - nw0;
   return t;
 }
 
 template <int MODE>
-__device__ __forceinline__ void y_produce(const TmaStepArgs& A, Producer& pr, unsigned char* ring, uint64_t* full,
-                                          uint64_t* empty, const CUtensorMap* mG0, const CUtensorMap* mG1,
-                                          const CUtensorMap* mW0, const CUtensorMap* mW1, const CUtensorMap* mH,
-                                          double* fbuf, uint64_t* fempty) {
+__device__ __forceinline__ void y_issue(const TmaStepArgs& A, uint32_t gs, unsigned char* ring, uint64_t* full,
+                                        const CUtensorMap* mG0, const CUtensorMap* mG1, const CUtensorMap* mW0,
+                                        const CUtensorMap* mW1, const CUtensorMap* mH, double* fbuf) {
   const DirDev& y = A.P.s;
   const DirDev& x = A.P.o;
-  const int NST = A.nstages;
-  if (pr.tile >= A.ntiles) return;
-  const YTile t = y_decode(A, pr.tile);
+  const uint32_t tl = A.fS.div(gs);
+  const int s = A.S - 1 - (int)(gs - tl * A.S);
+  const int tile = blockIdx.x + (int)tl * gridDim.x;
+  if (tile >= A.ntiles) return;
+  const int slot = (int)(gs - A.fN.div(gs) * A.nstages);
+  const YTile t = y_decode(A, tile);
   const int e0 = t.g * A.EG, kh0 = t.kw * A.R;
   const int hL = x.bc == 0 ? t.e_x - 1 : t.e_x;
-  const int slot = pr.slot;
-  if (pr.round >= 1) mbar_wait(&empty[slot], (pr.round - 1) & 1);
   unsigned char* st = ring + (size_t)slot * A.stage_bytes;
-  if (pr.first) {  // chain factors of the tile's EG elements x 2 parities (one contiguous block)
-    const uint32_t fb = pr.tt & 1;
-    if (pr.tt >= 2) mbar_wait(&fempty[fb], ((pr.tt >> 1) - 1) & 1);
+  if (s == A.S - 1) {  // chain factors of the tile's EG elements x 2 parities (one contiguous block)
+    const uint32_t fb = tl & 1;
     const int ne = (y.n - e0) < A.EG ? (y.n - e0) : A.EG;
     const uint32_t fbytes = 2 * ne * A.P.f.cfs * 8;
     const int mx = chain_len(x.p, 0), rows = (mx - kh0) < A.R ? (mx - kh0) : A.R;
@@ -355,22 +360,11 @@ __device__ __forceinline__ void y_produce(const TmaStepArgs& A, Producer& pr, un
   } else {
     mbar_expect_tx(&full[slot], A.tx_bytes);
   }
-  const int k0 = 2 * KCP * pr.s;
+  const int k0 = 2 * KCP * s;
   if (MODE != ST_CORR) tma_load_4d(st, t.pi ? mG1 : mG0, &full[slot], k0, e0, t.e_x, kh0);
   if (MODE != ST_NONE) {
     tma_load_4d(st + A.off_w, t.pi ? mW1 : mW0, &full[slot], k0, e0, t.e_x, kh0 - 1);
     tma_load_3d(st + A.off_h, mH, &full[slot], k0, e0, hL);
-  }
-  if (++pr.slot == NST) {
-    pr.slot = 0;
-    ++pr.round;
-  }
-  pr.first = false;
-  if (--pr.s < 0) {
-    pr.tile += gridDim.x;
-    ++pr.tt;
-    pr.first = true;
-    pr.s = (chain_len(y.p, 0) - 1) / KCP;
   }
 }
 
@@ -388,39 +382,25 @@ __global__ void __launch_bounds__(NT, 1)
   unsigned char* ring = smem_raw;
   double* obuf = reinterpret_cast<double*>(smem_raw + A.out_off);  // 2 x NW x [RW][EG][16]
   double* fbuf = reinterpret_cast<double*>(smem_raw + A.fac_off);   // 2 x [EG][2][cfs]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.wb_off + 2 * A.wb_doubles * sizeof(double));
-  uint64_t* empty = full + NST;
-  uint64_t* fempty = empty + NST;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.bar_off);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(full + NST);
   const int lane = threadIdx.x & 31;
   const int EG = A.EG, R = A.R;
   const int my = chain_len(y.p, 0);
-  const int nst_tile = (my - 1) / KCP + 1;
-  Producer pr;
+  if (threadIdx.x < NST) cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
-    for (int k = 0; k < NST; ++k) {
-      mbar_init(&full[k], 1);
-      mbar_init(&empty[k], NW);
-    }
-    mbar_init(&fempty[0], NW);
-    mbar_init(&fempty[1], NW);
+    for (int k = 0; k < NST; ++k) mbar_init(&full[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    pr.tile = blockIdx.x;
-    pr.slot = 0;
-    pr.round = 0;
-    pr.tt = 0;
-    pr.first = true;
-    pr.s = nst_tile - 1;
-    for (int k = 0; k < NST; ++k) y_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH, fbuf, fempty);
-  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NST; ++k) y_issue<MODE>(A, k, ring, full, &mG0, &mG1, &mW0, &mW1, &mH, fbuf);
   // thread -> (row r of the window, y-parity py, y-element eo)
   const int tid = threadIdx.x;
   const int eo = tid % EG, py = (tid / EG) & 1, r = tid / (2 * EG);
   const int cfs = P.f.cfs;
   int cslot = 0;
-  uint32_t cround = 0, ctt = 0;
+  uint32_t cround = 0, ctt = 0, gs = 0;
   int ob = 0;  // output staging buffer parity
   for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++ctt) {
     const YTile t = y_decode(A, tile);
@@ -473,12 +453,13 @@ __global__ void __launch_bounds__(NT, 1)
           rv[u] = v;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (lane == 0 && release_is_last(cnt, slot))
+          y_issue<MODE>(A, gs + NST, ring, full, &mG0, &mG1, &mW0, &mW1, &mH, fbuf);
+        ++gs;
         if (++cslot == NST) {
           cslot = 0;
           ++cround;
         }
-        if (threadIdx.x == 0) y_produce<MODE>(A, pr, ring, full, empty, &mG0, &mG1, &mW0, &mW1, &mH, fbuf, fempty);
 #pragma unroll
         for (int u = KCP - 1; u >= 0; --u) {
           const int c = KCP * sg + u;
@@ -517,12 +498,9 @@ __global__ void __launch_bounds__(NT, 1)
         ob ^= 1;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&fempty[ctt & 1]);
   }
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
-
 /* ------------------------------------------------------------------ */
 /* precomputed stencil weights of the bubble lines (one ST_APPLY step)  */
 /* ------------------------------------------------------------------ */
@@ -812,24 +790,21 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
     A.tx_bytes = gb + wb + hb;
     A.fac_doubles = (P.f.cfs + 15) & ~15;
     A.wb_doubles = P.wtab ? A.EG * 5 * P.lay.Q : 0;
+    A.S = (chain_len(x.p, 0) - 1) / KR + 1;
     A.nstages = (budget - 2 * A.fac_doubles * 8 - 2 * A.wb_doubles * 8) / A.stage_bytes;
-    if (A.nstages > 32) A.nstages = 32;
-    // the producer (thread 0, also a consumer) must never reach the tile after
-    // next: it would wait on a factor buffer its own warp has not released
-    {
-      int mins = (chain_len(x.p, 0) - 1) / KR + 1;
-      if (chain_len(x.p, 1) > 0) {
-        const int s1 = (chain_len(x.p, 1) - 1) / KR + 1;
-        if (s1 < mins) mins = s1;
-      }
-      if (A.nstages > mins) A.nstages = mins;
-    }
-    if (A.nstages > env_int("HPFEM_NST_X", 3)) A.nstages = env_int("HPFEM_NST_X", 3);  // 3 measured best
+    if (A.nstages > env_int("HPFEM_NST_X", 4)) A.nstages = env_int("HPFEM_NST_X", 4);  // 4 measured best
+    if (A.nstages > A.S) A.nstages = A.S;  // the factor double buffer relies on NST <= S
     if (A.nstages < 1) A.nstages = 1;
     A.fac_off = A.nstages * A.stage_bytes;
     A.wb_off = A.fac_off + 2 * A.fac_doubles * 8;
-    A.ntiles = ((y.n + A.EG - 1) / A.EG) * x.n * 2;
-    const size_t smem = (size_t)A.wb_off + 2 * A.wb_doubles * 8 + (2 * A.nstages + 2) * sizeof(uint64_t);
+    A.bar_off = A.wb_off + 2 * A.wb_doubles * 8;
+    const int ngroups = (y.n + A.EG - 1) / A.EG;
+    A.ntiles = ngroups * x.n * 2;
+    A.fS = make_fdiv(A.S);
+    A.fN = make_fdiv(A.nstages);
+    A.fG = make_fdiv(ngroups);
+    A.fT = make_fdiv(x.n);
+    const size_t smem = (size_t)A.bar_off + 2 * A.nstages * sizeof(uint64_t);
     const int grid = A.ntiles < T->sms ? A.ntiles : T->sms;
     const int cl = chain_len(x.p, 0);
     const CUtensorMap* g = T->xv[gi];
@@ -854,17 +829,23 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
   const int obytes = 2 * NW * 256 * 8;
   A.fac_doubles = (2 * A.EG * P.f.cfs + 15) & ~15;
   A.wb_doubles = P.wtab ? ((A.R * 6 + 15) & ~15) : 0;
+  A.S = (chain_len(y.p, 0) - 1) / KCP + 1;
   A.nstages = (budget - obytes - 2 * A.fac_doubles * 8 - 2 * A.wb_doubles * 8) / A.stage_bytes;
-  if (A.nstages > 32) A.nstages = 32;
-  if (A.nstages > (chain_len(y.p, 0) - 1) / KCP + 1) A.nstages = (chain_len(y.p, 0) - 1) / KCP + 1;  // see x-solve
-  if (A.nstages > env_int("HPFEM_NST_Y", 99)) A.nstages = env_int("HPFEM_NST_Y", 99);
+  if (A.nstages > env_int("HPFEM_NST_Y", 4)) A.nstages = env_int("HPFEM_NST_Y", 4);
+  if (A.nstages > A.S) A.nstages = A.S;  // see x-solve
   if (A.nstages < 1) A.nstages = 1;
   A.out_off = A.nstages * A.stage_bytes;
   A.fac_off = A.out_off + obytes;
   A.wb_off = A.fac_off + 2 * A.fac_doubles * 8;
-  const int nw = (chain_len(x.p, 0) + A.R - 1) / A.R + (chain_len(x.p, 1) + A.R - 1) / A.R;
-  A.ntiles = ((y.n + A.EG - 1) / A.EG) * x.n * nw;
-  const size_t smem = (size_t)A.wb_off + 2 * A.wb_doubles * 8 + (2 * A.nstages + 2) * sizeof(uint64_t);
+  A.bar_off = A.wb_off + 2 * A.wb_doubles * 8;
+  A.nwt = (chain_len(x.p, 0) + A.R - 1) / A.R + (chain_len(x.p, 1) + A.R - 1) / A.R;
+  const int ngroups = (y.n + A.EG - 1) / A.EG;
+  A.ntiles = ngroups * x.n * A.nwt;
+  A.fS = make_fdiv(A.S);
+  A.fN = make_fdiv(A.nstages);
+  A.fG = make_fdiv(ngroups);
+  A.fT = make_fdiv(A.nwt);
+  const size_t smem = (size_t)A.bar_off + 2 * A.nstages * sizeof(uint64_t);
   const int grid = A.ntiles < T->sms ? A.ntiles : T->sms;
   const int cl = chain_len(y.p, 0);
   switch (P.mode) {
