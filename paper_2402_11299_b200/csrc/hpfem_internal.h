@@ -133,6 +133,12 @@ struct StepParams {
   FacView f;  // factor of this solve
   double* out;
   const double* wtab;  // precomputed stencil weights of the bubble lines (TMA kernels; null = build in-kernel)
+  /* element-major layout only (null otherwise): compact copy of the
+   * chain-first bubbles (k = 0, 1) of every y-element, [row][n_y][2], i.e.
+   * the only bubbles the y-hat rows of the stencil and the hat Schur
+   * right-hand side touch -- contiguous instead of 16 bytes out of every Q. */
+  double* z01;         // y-solves: written for every row of out
+  const double* z01p;  // x-solves: the copy belonging to Xp
 };
 
 /* launchers (kernels.cu); return cudaError_t of the launch */

@@ -484,6 +484,22 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
     double rh = rhs_at<DIR>(G, P.alphaG, Xp, st, li, t, ld);
     const int node = node_of_hat(t, s.bc);
     const int eL = node - 1, eR = node;
+    if (DIR == 1 && P.z01) {  // chain-first bubbles from the compact copy
+      const double* zr = P.z01 + (size_t)li * 2 * n;
+      if (eL >= 0) {
+        const double dl = s.delta[eL];
+        const double2 v = *reinterpret_cast<const double2*>(zr + 2 * eL);
+        rh -= s_hat_bub(S, dl, 1, 0) * v.x;
+        if (k1) rh -= s_hat_bub(S, dl, 1, 1) * v.y;
+      }
+      if (eR <= n - 1) {
+        const double dr = s.delta[eR];
+        const double2 v = *reinterpret_cast<const double2*>(zr + 2 * eR);
+        rh -= s_hat_bub(S, dr, 0, 0) * v.x;
+        if (k1) rh -= s_hat_bub(S, dr, 0, 1) * v.y;
+      }
+      return rh;
+    }
     if (eL >= 0) {
       const double dl = s.delta[eL];
       rh -= s_hat_bub(S, dl, 1, 0) * out_r[addr<DIR>(li, spos_bub<DIR>(P, 0, eL), ld)];
@@ -721,6 +737,9 @@ __global__ void __launch_bounds__(128) k_hatrows_y(StepParams P) {
     const int e = j / L.Q, k = j - e * L.Q;
     if (k < y.p - 1) out[j] = seg[j];
   }
+  if (P.z01)  // chain-first bubbles: compact copy
+    for (int j = threadIdx.x; j < 2 * ne; j += blockDim.x)
+      P.z01[(size_t)t * 2 * y.n + 2 * e0 + j] = seg[(j >> 1) * L.Q + (j & 1)];
 }
 
 /* x-solve, lines = y-hat columns: CTA = (x-element e_x, parity pi, group
@@ -744,7 +763,7 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
   const int elo = max(node0 - 1, 0);
   const int ehi = min(node_of_hat(l0 + nl - 1, y.bc), y.n - 1);
   const int nE = ehi - elo + 1;
-  const int RW = TC + HREG + 2 * (TC + 2);  // per row: G | hats | bubble 0 | bubble 1 (16-byte aligned parts)
+  const int RW = TC + HREG + 2 * (TC + 2);  // per row: G | hats | bubbles 0/1 of elo..ehi, interleaved (16-byte aligned parts)
   double* rows = sh;                             // [m][RW]
   const int cfs = P.f.cfs;
   double* fac = sh + (size_t)m * RW;             // [cfs]
@@ -760,16 +779,20 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
   const bool useG = P.alphaG != 0.0, useW = P.mode != ST_NONE;
   const int hs = hlo < 0 ? 0 : hlo;              // first hat column actually copied (hats < 0 do not exist)
   const int nh_c = min(l0 + nl + 1 - hs, y.nh - hs);  // hats hs .. l0+nl (the last line's right neighbour)
+  const bool zc = useW && P.z01p;  // bubbles 0/1 from the compact copy (bulk) instead of 16-byte gathers
   if (threadIdx.x == 0) {
     uint32_t bytes = cfs * 8;
     const uint32_t gb = useG ? ((nl * 8 + 15) & ~15) : 0;
     const uint32_t hb = useW ? ((nh_c * 8 + 15) & ~15) : 0;
-    bytes += m * (gb + hb);
+    const uint32_t zb = zc ? nE * 16 : 0;
+    bytes += m * (gb + hb + zb);
     mbar_expect_tx(&bar, bytes);
     for (int c = 0; c < m; ++c) {
-      const size_t row = (size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld;
+      const size_t rix = (size_t)(x.nh + (pi + 2 * c) * x.n + e_x);
+      const size_t row = rix * P.ld;
       if (gb) bulk_load(rows + (size_t)c * RW, P.G + row + l0, gb, &bar);
       if (hb) bulk_load(rows + (size_t)c * RW + TC + (hs - hlo), P.Xp + row + hs, hb, &bar);
+      if (zb) bulk_load(rows + (size_t)c * RW + TC + HREG, P.z01p + rix * 2 * y.n + 2 * elo, zb, &bar);
     }
     bulk_load(fac, P.f.cf + (size_t)(2 * e_x + pi) * cfs, cfs * 8, &bar);
   }
@@ -781,7 +804,7 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
   else if (hs > hlo)  // the staged slots before hat 0 must read as zero
     for (int c = threadIdx.x; c < m; c += blockDim.x)
       for (int j = 0; j < hs - hlo; ++j) rows[(size_t)c * RW + TC + j] = 0.0;
-  {
+  if (!zc) {
     const int nb = m * (TC + 2);  // (row, element) pairs, 2 doubles each
 #pragma unroll 4
     for (int idx = threadIdx.x; idx < nb; idx += blockDim.x) {
@@ -793,8 +816,8 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
         if (y.p - 2 < 1) v.y = 0.0;
       }
       double* R = rows + (size_t)c * RW + TC + HREG;
-      R[ei] = v.x;              // bubble 0
-      R[(TC + 2) + ei] = v.y;   // bubble 1
+      R[2 * ei] = v.x;      // bubble 0
+      R[2 * ei + 1] = v.y;  // bubble 1
     }
   }
   mbar_wait(&bar, 0);
@@ -814,7 +837,7 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
         off[q] = TC + (d - hlo);
       } else {
         const int b = d - y.nh, k = b / y.n, e = b - k * y.n;
-        off[q] = TC + HREG + k * (TC + 2) + (e - elo);
+        off[q] = TC + HREG + 2 * (e - elo) + k;
       }
     }
     const double aG = P.alphaG;

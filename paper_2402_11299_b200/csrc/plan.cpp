@@ -259,6 +259,7 @@ struct hpfem_plan_s {
   double* Gp = nullptr;           // internal copy of G
   double* X1 = nullptr;           // W_{j-1/2} (deferred along y), final y-solve
   double* X2 = nullptr;           // W_j (deferred along x)
+  double* Z01 = nullptr;          // chain-first y-bubbles of X1, [row][n_y][2] (element-major layout only)
   TmaPlan* tma = nullptr;         // TMA tensor maps over {Gp, X1, X2} (null = LDG kernels only)
   double* wx = nullptr;           // precomputed x-solve stencil weights, J tables
   double* wy = nullptr;           // precomputed y-solve stencil weights, J tables (table 0 unused)
@@ -310,6 +311,7 @@ void free_plan(hpfem_plan_t pl) {
   cudaFree(pl->Gp);
   cudaFree(pl->X1);
   cudaFree(pl->X2);
+  cudaFree(pl->Z01);
   cudaFree(pl->wx);
   cudaFree(pl->wy);
   delete pl;
@@ -420,6 +422,11 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
     for (double** b : {&pl->Gp, &pl->X1, &pl->X2}) {
       if ((ce = cudaMalloc(b, bytes)) != cudaSuccess) return fail_cuda(ce, "alloc workspace");
       if ((ce = cudaMemsetAsync(*b, 0, bytes, st)) != cudaSuccess) return fail_cuda(ce, "memset workspace");
+    }
+    if (pl->use_tma) {
+      const size_t zb = sizeof(double) * ((size_t)hx.N * 2 * pl->dy.n + 64);
+      if ((ce = cudaMalloc(&pl->Z01, zb)) != cudaSuccess) return fail_cuda(ce, "alloc workspace");
+      if ((ce = cudaMemsetAsync(pl->Z01, 0, zb, st)) != cudaSuccess) return fail_cuda(ce, "memset workspace");
     }
     double* const arrays[3] = {pl->Gp, pl->X1, pl->X2};
     pl->tma = tma_plan_create(pl->dx, pl->dy, pl->lay, arrays, pl->use_tma);
@@ -610,6 +617,7 @@ int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, vo
     A.alphaG = 1.0;
     A.f = fview(pl, 1, j);
     A.out = pl->X1;
+    A.z01 = pl->Z01;
     if (j == 0) {
       A.mode = ST_NONE;  // W_0 = 0
     } else {
@@ -631,6 +639,7 @@ int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, vo
     B.out = pl->X2;
     B.mode = ST_APPLY;
     B.Xp = pl->X1;
+    B.z01p = pl->Z01;
     B.kap_a = 1.0;
     B.tau = hw2 + pl->Q[j];
     B.cvL = A.f.vL;
@@ -644,6 +653,7 @@ int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, vo
   Fin.alphaG = 0.0;
   Fin.f = fview(pl, 1, pl->J);
   Fin.out = pl->X1;
+  Fin.z01 = pl->Z01;
   Fin.mode = ST_CORR;
   Fin.Xp = pl->X2;
   const FacView last = fview(pl, 0, iters - 1);

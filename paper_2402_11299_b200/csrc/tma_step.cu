@@ -488,6 +488,8 @@ __global__ void __launch_bounds__(NT, 1)
           z = live ? zn : z;
           const double zv = live ? zn : 0.0;
           o[((r - wr0) * EG + eo) * 16 + py + 2 * u] = zv;
+          if (sg == 0 && u == 0 && live && P.z01)  // chain-first bubble (degree py): compact copy
+            P.z01[(size_t)(x.nh + kx * x.n + e_x) * (2 * y.n) + 2 * ey + py] = zn;
         }
         fence_proxy_async();
         __syncwarp();
