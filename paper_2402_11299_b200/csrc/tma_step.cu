@@ -127,7 +127,13 @@ constexpr int NT = 256;    // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int KR = 8;      // x-solve: chain positions (rows) per stage
 constexpr int KCP = 8;     // y-solve: chain positions per stage (16 degrees)
-constexpr int KBOX = 18;   // y-solve: degrees per box row (16 + 2 to spread smem banks)
+constexpr int KBOX = 16;   // y-solve: degrees per box row (one 128-byte line, 128B-swizzled in smem)
+
+/* y-solve boxes are 128-byte rows stored with the TMA 128B swizzle: the
+ * 16-byte chunk j of box row rho sits at chunk j ^ (rho & 7), so the lanes of
+ * a warp (different rows rho = (row, element), same degree) hit different
+ * banks.  Offset in doubles of degree (py + 2u) of box row rho: */
+__device__ __forceinline__ int swz(int rho, int u, int py) { return rho * 16 + ((u ^ (rho & 7)) << 1) + py; }
 
 /* Ring discipline.  Every tile of a launch has the same number S of stages
  * and this CTA's stages are numbered gs = 0, 1, ... in consumption order
@@ -374,7 +380,7 @@ __global__ void __launch_bounds__(NT, 1)
                 const __grid_constant__ CUtensorMap mW0, const __grid_constant__ CUtensorMap mW1,
                 const __grid_constant__ CUtensorMap mH, const __grid_constant__ CUtensorMap mO0,
                 const __grid_constant__ CUtensorMap mO1) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   const StepParams& P = A.P;
   const DirDev& y = P.s;  // solve direction
   const DirDev& x = P.o;  // apply direction
@@ -389,6 +395,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int my = chain_len(y.p, 0);
   if (threadIdx.x < NST) cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
+    if (su32(smem_raw) & 1023) __trap();  // the 128B swizzle needs 1024-byte aligned boxes
     for (int k = 0; k < NST; ++k) mbar_init(&full[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -421,12 +428,12 @@ __global__ void __launch_bounds__(NT, 1)
       for (int k = 0; k < 5; ++k) st.w[k] = 0.0;
     }
     const int rr = r < R ? r : 0;
-    const int og = (rr * EG + eo) * KBOX + py;          // G box [R][EG][KBOX]
-    const int ow1 = (rr * EG + eo) * KBOX + py;         // W box [R+2][EG][KBOX]: row k_x - 2
-    const int ow0 = ((rr + 1) * EG + eo) * KBOX + py;   //   k_x
-    const int ow2 = ((rr + 2) * EG + eo) * KBOX + py;   //   k_x + 2
-    const int oh0 = eo * KBOX + py;                     // hat box [2][EG][KBOX]: hL
-    const int oh1 = (EG + eo) * KBOX + py;              //   hR
+    const int rg = rr * EG + eo;        // G box [R][EG][16]: box row of (r, eo)
+    const int rw1 = rr * EG + eo;       // W box [R+2][EG][16]: row k_x - 2
+    const int rw0 = (rr + 1) * EG + eo; //   k_x
+    const int rw2 = (rr + 2) * EG + eo; //   k_x + 2
+    const int rh0 = eo;                 // hat box [2][EG][16]: hL
+    const int rh1 = EG + eo;            //   hR
     double ys[CL];
     double yv = 0.0;
 #pragma unroll
@@ -446,10 +453,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int u = 0; u < KCP; ++u) {
           double v = 0.0;
-          if (MODE != ST_CORR) v = Gs[og + 2 * u];
+          if (MODE != ST_CORR) v = Gs[swz(rg, u, py)];
           if (MODE != ST_NONE)
-            v += st.w[0] * Ws[ow0 + 2 * u] + st.w[1] * Ws[ow1 + 2 * u] + st.w[2] * Ws[ow2 + 2 * u] +
-                 st.w[3] * Hs[oh0 + 2 * u] + st.w[4] * Hs[oh1 + 2 * u];
+            v += st.w[0] * Ws[swz(rw0, u, py)] + st.w[1] * Ws[swz(rw1, u, py)] + st.w[2] * Ws[swz(rw2, u, py)] +
+                 st.w[3] * Hs[swz(rh0, u, py)] + st.w[4] * Hs[swz(rh1, u, py)];
           rv[u] = v;
         }
         __syncwarp();
@@ -487,7 +494,7 @@ __global__ void __launch_bounds__(NT, 1)
           const bool live = valid && c < mthr;
           z = live ? zn : z;
           const double zv = live ? zn : 0.0;
-          o[((r - wr0) * EG + eo) * 16 + py + 2 * u] = zv;
+          o[swz((r - wr0) * EG + eo, u, py)] = zv;
           if (sg == 0 && u == 0 && live && P.z01)  // chain-first bubble (degree py): compact copy
             P.z01[(size_t)(x.nh + kx * x.n + e_x) * (2 * y.n) + 2 * ey + py] = zn;
         }
@@ -564,7 +571,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 static bool encode(CUtensorMap* m, int rank, void* base, const uint64_t* dims, const uint64_t* strides_bytes,
-                   const uint32_t* box) {
+                   const uint32_t* box, bool swizzle128 = false) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t d[5], s[4];
@@ -576,7 +583,7 @@ static bool encode(CUtensorMap* m, int rank, void* base, const uint64_t* dims, c
     if (i < rank - 1) s[i] = strides_bytes[i];
   }
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base, d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -690,17 +697,17 @@ TmaPlan* tma_plan_create(const DirDev& x, const DirDev& y, const Layout& L, doub
         const uint64_t s4[3] = {Q8, ld8, 2 * (uint64_t)x.n * ld8};
         const uint32_t bG[4] = {KBOX, (uint32_t)EG, 1, (uint32_t)R};
         const uint32_t bW[4] = {KBOX, (uint32_t)EG, 1, (uint32_t)R + 2};
-        ok = encode(&T->yG[a][pi], 4, base, d4, s4, bG) && encode(&T->yW[a][pi], 4, base, d4, s4, bW);
+        ok = encode(&T->yG[a][pi], 4, base, d4, s4, bG, true) && encode(&T->yW[a][pi], 4, base, d4, s4, bW, true);
         if (ok && a == 1) {
           const uint32_t bO[4] = {16, (uint32_t)EG, 1, (uint32_t)RW};
-          ok = encode(&T->yO[pi], 4, base, d4, s4, bO);
+          ok = encode(&T->yO[pi], 4, base, d4, s4, bO, true);
         }
       }
       if (ok) {
         const uint64_t d3[3] = {(uint64_t)L.Q, (uint64_t)y.n, (uint64_t)x.N};
         const uint64_t s3[2] = {Q8, ld8};
         const uint32_t b3[3] = {KBOX, (uint32_t)EG, 2};
-        ok = encode(&T->yH[a], 3, arrays[a] + L.hb, d3, s3, b3);
+        ok = encode(&T->yH[a], 3, arrays[a] + L.hb, d3, s3, b3, true);
       }
     }
   }
@@ -715,7 +722,7 @@ bool tma_supports(const TmaPlan* T, int dir) { return T && T->ok && (dir == 0 ||
 /* The dynamic shared-memory opt-in is set once per kernel instantiation:
  * cudaFuncSetAttribute can serialise with in-flight launches of the same
  * kernel, which would stall the host between half-steps. */
-constexpr int SMEM_OPTIN = 200 * 1024;
+constexpr int SMEM_OPTIN = 227 * 1024;  // the sm_100 per-CTA maximum
 
 template <typename K>
 static cudaError_t optin(K k, bool& done) {
@@ -767,6 +774,7 @@ static cudaError_t dispatch_y(int cl, const TmaStepArgs& A, const TmaPlan* T, in
 }
 
 static int round128(int b) { return (b + 127) & ~127; }
+static int round1024(int b) { return (b + 1023) & ~1023; }
 
 /* Launch the bubble-line part of one half-step.  ia_g / ia_w: indices of the
  * G and Xp arrays among (Gp, X1, X2) (-1 when unused). */
@@ -824,9 +832,9 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
   const int gb = (P.mode != ST_CORR) ? A.R * A.EG * KBOX * 8 : 0;
   const int wb = (P.mode != ST_NONE) ? (A.R + 2) * A.EG * KBOX * 8 : 0;
   const int hb = (P.mode != ST_NONE) ? 2 * A.EG * KBOX * 8 : 0;
-  A.off_w = round128(gb);
-  A.off_h = A.off_w + round128(wb);
-  A.stage_bytes = round128(A.off_h + hb);
+  A.off_w = round1024(gb);  // swizzled boxes: 1024-byte aligned
+  A.off_h = A.off_w + round1024(wb);
+  A.stage_bytes = round1024(A.off_h + hb);
   A.tx_bytes = gb + wb + hb;
   const int obytes = 2 * NW * 256 * 8;
   A.fac_doubles = (2 * A.EG * P.f.cfs + 15) & ~15;
