@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
     if (l >= 0) {
       Stencil st;
       line_stencil<DIR>(P, l, st);
+#pragma unroll 4
       for (int t = tg; t < nh; t += ng) sh[t * LB + j] = rhs_hat(st, li, t);
     }
   } else {
@@ -534,24 +535,62 @@ __global__ void __launch_bounds__(256) k_hats(StepParams P) {
       for (int t = lane; t < nh; t += 32) sh[t * LB + j] = rhs_hat(st, l, t);
     }
   }
+  // hat factors to shared memory (every solver thread reads the same entry: broadcast)
+  double* fil = sh + (size_t)nh * LB;
+  double* fg = fil + nh;
+  for (int t = threadIdx.x; t < nh; t += blockDim.x) {
+    fil[t] = __ldg(P.f.ilh + t);
+    fg[t] = __ldg(P.f.gh + t);
+  }
   __syncthreads();
-  // sequential tridiagonal reverse-Cholesky solve per line, in shared memory
+  // sequential tridiagonal reverse-Cholesky solve per line, in shared memory;
+  // loads batched HB positions ahead so that only the dependent FMA
+  //   y_t = il_t r_t - (g_t il_t) y_{t+1},   x_t = il_t y_t - (g_{t-1} il_t) x_{t-1}
+  // is on the critical path
   const int nlines = DIR == 0 ? ld : P.o.N;
   if (threadIdx.x < LB && l0 + (int)threadIdx.x < nlines &&
       (DIR == 1 || ydof_of_col(P.lay, P.o, l0 + (int)threadIdx.x) >= 0)) {
-    const int j = threadIdx.x;
-    const double* __restrict__ ilh = P.f.ilh;
-    const double* __restrict__ gh = P.f.gh;
+    constexpr int HB = 8;
+    double* v = sh + threadIdx.x;  // v[t * LB]
     double y = 0.0;
-    for (int t = nh - 1; t >= 0; --t) {
-      y = (sh[t * LB + j] - __ldg(gh + t) * y) * __ldg(ilh + t);
-      sh[t * LB + j] = y;
+    int t = nh - 1;
+    for (; t >= HB - 1; t -= HB) {
+      double a[HB], b[HB];
+#pragma unroll
+      for (int u = 0; u < HB; ++u) {
+        const double il = fil[t - u];
+        a[u] = il * v[(t - u) * LB];
+        b[u] = fg[t - u] * il;
+      }
+#pragma unroll
+      for (int u = 0; u < HB; ++u) {
+        y = fma(-b[u], y, a[u]);
+        v[(t - u) * LB] = y;
+      }
     }
-    double x = 0.0, gp = 0.0;
-    for (int t = 0; t < nh; ++t) {
-      x = (sh[t * LB + j] - gp * x) * __ldg(ilh + t);
-      gp = __ldg(gh + t);
-      sh[t * LB + j] = x;
+    for (; t >= 0; --t) {
+      y = fma(-fg[t] * fil[t], y, fil[t] * v[t * LB]);
+      v[t * LB] = y;
+    }
+    double x = 0.0;
+    t = 0;
+    for (; t + HB <= nh; t += HB) {
+      double a[HB], b[HB];
+#pragma unroll
+      for (int u = 0; u < HB; ++u) {
+        const double il = fil[t + u];
+        a[u] = il * v[(t + u) * LB];
+        b[u] = (t + u > 0 ? fg[t + u - 1] : 0.0) * il;
+      }
+#pragma unroll
+      for (int u = 0; u < HB; ++u) {
+        x = fma(-b[u], x, a[u]);
+        v[(t + u) * LB] = x;
+      }
+    }
+    for (; t < nh; ++t) {
+      x = fma(-(t > 0 ? fg[t - 1] : 0.0) * fil[t], x, fil[t] * v[t * LB]);
+      v[t * LB] = x;
     }
   }
   __syncthreads();
@@ -620,7 +659,7 @@ cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st) {
 
 template <int DIR, int LB>
 static cudaError_t launch_hats_lb(const StepParams& P, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (size_t)P.s.nh * LB;
+  const size_t smem = sizeof(double) * (size_t)P.s.nh * (LB + 2);
   static size_t opted = 48 * 1024;
   if (smem > opted) {
     cudaError_t e = cudaFuncSetAttribute(k_hats<DIR, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -638,7 +677,7 @@ static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
   static int lb = -1;
   if (lb < 0) {
     const char* v = getenv(DIR == 0 ? "HPFEM_HAT_LB_X" : "HPFEM_HAT_LB_Y");
-    lb = v && *v ? atoi(v) : (DIR == 0 ? 32 : 8);
+    lb = v && *v ? atoi(v) : 32;
   }
   return lb == 8 ? launch_hats_lb<DIR, 8>(P, st) : launch_hats_lb<DIR, 32>(P, st);
 }
@@ -654,6 +693,53 @@ static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
  * smem: 8 row segments [EGH*Q] (G + 7 stencil rows) and the chains'
  * factors [EGH][2][cfs]. */
 constexpr int EGH = 8;
+
+/* In-place solve of one bubble chain held in shared memory, v[c * vs],
+ * c < m, with the chain-major factors f ([4c] il, [4c+1] g il, [4c+2]
+ * g_prev il): y_c = il_c v_c - hd_c y_{c+1} downwards, then z_c = il_c y_c -
+ * hu_c z_{c-1} upwards.  Loads are batched CB positions ahead of the
+ * dependent FMAs (the compiler cannot hoist them over the stores itself). */
+__device__ __forceinline__ void chain_solve_smem(const double* f, double* v, int vs, int m) {
+  constexpr int CB = 8;
+  double y = 0.0;
+  int c = m - 1;
+  for (; c >= CB - 1; c -= CB) {
+    double a[CB], b[CB];
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      a[u] = f[4 * (c - u)] * v[(c - u) * vs];
+      b[u] = f[4 * (c - u) + 1];
+    }
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      y = fma(-b[u], y, a[u]);
+      v[(c - u) * vs] = y;
+    }
+  }
+  for (; c >= 0; --c) {
+    y = fma(-f[4 * c + 1], y, f[4 * c] * v[c * vs]);
+    v[c * vs] = y;
+  }
+  double z = 0.0;
+  c = 0;
+  for (; c + CB <= m; c += CB) {
+    double a[CB], b[CB];
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      a[u] = f[4 * (c + u)] * v[(c + u) * vs];
+      b[u] = f[4 * (c + u) + 2];
+    }
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      z = fma(-b[u], z, a[u]);
+      v[(c + u) * vs] = z;
+    }
+  }
+  for (; c < m; ++c) {
+    z = fma(-f[4 * c + 2], z, f[4 * c] * v[c * vs]);
+    v[c * vs] = z;
+  }
+}
 
 __global__ void __launch_bounds__(128) k_hatrows_y(StepParams P) {
   extern __shared__ double sh[];
@@ -720,16 +806,7 @@ __global__ void __launch_bounds__(128) k_hatrows_y(StepParams P) {
     const int m = chain_len(y.p, pi);
     const double* f = fac + (eo * 2 + pi) * cfs;
     double* v = seg + eo * L.Q + pi;
-    double yv = 0.0;
-    for (int c = m - 1; c >= 0; --c) {
-      yv = fma(-f[4 * c + 1], yv, f[4 * c] * v[2 * c]);
-      v[2 * c] = yv;
-    }
-    double z = 0.0;
-    for (int c = 0; c < m; ++c) {
-      z = fma(-f[4 * c + 2], z, f[4 * c] * v[2 * c]);
-      v[2 * c] = z;
-    }
+    chain_solve_smem(f, v, 2, m);
   }
   __syncthreads();
   double* out = P.out + (size_t)t * P.ld + col0;
@@ -780,21 +857,22 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
   const int hs = hlo < 0 ? 0 : hlo;              // first hat column actually copied (hats < 0 do not exist)
   const int nh_c = min(l0 + nl + 1 - hs, y.nh - hs);  // hats hs .. l0+nl (the last line's right neighbour)
   const bool zc = useW && P.z01p;  // bubbles 0/1 from the compact copy (bulk) instead of 16-byte gathers
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0 issues the copies, one row per lane
     uint32_t bytes = cfs * 8;
     const uint32_t gb = useG ? ((nl * 8 + 15) & ~15) : 0;
     const uint32_t hb = useW ? ((nh_c * 8 + 15) & ~15) : 0;
     const uint32_t zb = zc ? nE * 16 : 0;
     bytes += m * (gb + hb + zb);
-    mbar_expect_tx(&bar, bytes);
-    for (int c = 0; c < m; ++c) {
+    if (threadIdx.x == 0) mbar_expect_tx(&bar, bytes);
+    __syncwarp();
+    for (int c = threadIdx.x; c < m; c += 32) {
       const size_t rix = (size_t)(x.nh + (pi + 2 * c) * x.n + e_x);
       const size_t row = rix * P.ld;
       if (gb) bulk_load(rows + (size_t)c * RW, P.G + row + l0, gb, &bar);
       if (hb) bulk_load(rows + (size_t)c * RW + TC + (hs - hlo), P.Xp + row + hs, hb, &bar);
       if (zb) bulk_load(rows + (size_t)c * RW + TC + HREG, P.z01p + rix * 2 * y.n + 2 * elo, zb, &bar);
     }
-    bulk_load(fac, P.f.cf + (size_t)(2 * e_x + pi) * cfs, cfs * 8, &bar);
+    if (threadIdx.x == 0) bulk_load(fac, P.f.cf + (size_t)(2 * e_x + pi) * cfs, cfs * 8, &bar);
   }
   if (!useG)
     for (int idx = threadIdx.x; idx < m * TC; idx += blockDim.x) rows[(size_t)(idx / TC) * RW + idx % TC] = 0.0;
@@ -841,20 +919,16 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
       }
     }
     const double aG = P.alphaG;
-    double yv = 0.0;
-    for (int c = m - 1; c >= 0; --c) {
+    // right-hand sides in place (each thread reads its stencil columns and
+    // overwrites only its own G column), then the chain solve
+    for (int c = 0; c < m; ++c) {
       const double* R = rows + (size_t)c * RW;
       double r = aG != 0.0 ? aG * R[threadIdx.x] : 0.0;
 #pragma unroll
       for (int q = 0; q < 7; ++q) r += st.w[q] * R[off[q]];
-      yv = fma(-fac[4 * c + 1], yv, fac[4 * c] * r);
-      rows[(size_t)c * RW + threadIdx.x] = yv;
+      rows[(size_t)c * RW + threadIdx.x] = r;
     }
-    double z = 0.0;
-    for (int c = 0; c < m; ++c) {
-      z = fma(-fac[4 * c + 2], z, fac[4 * c] * rows[(size_t)c * RW + threadIdx.x]);
-      rows[(size_t)c * RW + threadIdx.x] = z;
-    }
+    chain_solve_smem(fac, rows + threadIdx.x, RW, m);
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < m * TC; idx += blockDim.x) {

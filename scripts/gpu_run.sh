@@ -1,7 +1,5 @@
-timeout 400 python -m pytest tests -m gpu -x -q -k "not config5" > gpurun_out/t19.log 2>&1; echo tests rc=$?
-tail -3 gpurun_out/t19.log
-for ny in 2 3 4; do
-HPFEM_NST_Y=$ny timeout 120 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b19_$ny.json 2>gpurun_out/b19_$ny.err
-python -c "import json;d=json.loads(open('gpurun_out/b19_$ny.json').read().strip().splitlines()[-1]);print($ny, round(d['ms_per_step'],1),d['roofline']['per_kind_ms'])"
-done
-ncu --metrics gpu__time_duration.sum --clock-control none -s 1500 -c 200 --csv --log-file gpurun_out/launches19.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu19.log 2>&1; echo ncu rc=$?
+timeout 400 python -m pytest tests -m gpu -x -q -k "not config5" > gpurun_out/t23.log 2>&1; echo tests rc=$?
+tail -3 gpurun_out/t23.log
+timeout 120 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b23.json 2>gpurun_out/b23.err
+python -c "import json;d=json.loads(open('gpurun_out/b23.json').read().strip().splitlines()[-1]);print(round(d['ms_per_step'],1),d['roofline']['per_kind_ms'])"
+ncu --metrics gpu__time_duration.sum --clock-control none -s 1500 -c 200 --csv --log-file gpurun_out/launches23.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu23.log 2>&1; echo ncu rc=$?
