@@ -20,7 +20,8 @@ LIB = os.path.join(HERE, "libhpfem_b200.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"] + \
+    os.environ.get("HPFEM_NVCC_EXTRA", "").split()  # experiments only
 CXX_FLAGS = ["-O2", "-std=gnu++17", "-fPIC", "-Wall", "-Wextra", f"-I{CUDA}/include"]
 
 
