@@ -23,8 +23,11 @@
  * P:L384) or p n + 1 (Neumann).
  *
  * Ownership: the caller owns F, U, F_leg (DEVICE pointers, e.g. torch
- * tensors).  The plan owns its factor tables, shift tables and one N_x x N_y
- * workspace.  All work is enqueued asynchronously on the stream passed in
+ * tensors).  The plan owns its factor tables, shift tables, stencil-weight
+ * tables and its workspace: three N_x x ld internal arrays (the plan's copy
+ * of G and the two ADI iterates, ld ~ N_y, internal column order, see
+ * DESIGN.md section 5) plus, on the TMA path, an N_x x 2 n_y side array.
+ * All work is enqueued asynchronously on the stream passed in
  * (a cudaStream_t; NULL = legacy default stream).  A plan may be used by one
  * stream at a time (its workspace is shared by its solves).
  *
