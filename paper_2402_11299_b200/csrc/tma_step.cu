@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
 
 #include "hpfem_internal.h"
 #include "ops1d.h"
@@ -127,6 +128,11 @@ constexpr int NT = 256;    // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int KR = 8;      // x-solve: chain positions (rows) per stage
 constexpr int KCP = 8;     // y-solve: chain positions per stage (16 degrees)
+constexpr int SPB = 2;     // y-solve: chain stages per output staging buffer (one proxy fence each)
+#ifndef HPFEM_NOBUF
+#define HPFEM_NOBUF 2
+#endif
+constexpr int NOBUF = HPFEM_NOBUF;  // y-solve: output staging buffers per warp
 constexpr int KBOX = 16;   // y-solve: degrees per box row (one 128-byte line, 128B-swizzled in smem)
 
 /* y-solve boxes are 128-byte rows stored with the TMA 128B swizzle: the
@@ -409,6 +415,9 @@ __global__ void __launch_bounds__(NT, 1)
   int cslot = 0;
   uint32_t cround = 0, ctt = 0, gs = 0;
   int ob = 0;  // output staging buffer parity
+#ifdef HPFEM_YPROF
+  long long t_w0 = 0, t_w = 0, t_bwd = 0, t_br = 0, t_fe = 0, t_all = clock64(), t0, t1;
+#endif
   for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++ctt) {
     const YTile t = y_decode(A, tile);
     const double* fb = fbuf + (ctt & 1) * A.fac_doubles + (eo * 2 + py) * cfs;  // this thread's chain
@@ -440,7 +449,14 @@ __global__ void __launch_bounds__(NT, 1)
     for (int sg = CL / KCP - 1; sg >= 0; --sg) {
       if (KCP * sg < my) {
         const int slot = cslot;
+#ifdef HPFEM_YPROF
+        t0 = clock64();
+#endif
         mbar_wait(&full[slot], cround & 1);
+#ifdef HPFEM_YPROF
+        t1 = clock64();
+        if (KCP * sg + KCP >= my) t_w0 += t1 - t0; else t_w += t1 - t0;
+#endif
         if (wtab && KCP * sg + KCP >= my) {  // first stage of the tile: the weights have landed
 #pragma unroll
           for (int k = 0; k < 5; ++k) st.w[k] = valid ? wb[r * 6 + k] : 0.0;
@@ -478,37 +494,71 @@ __global__ void __launch_bounds__(NT, 1)
     }
     // upward sweep, staged per warp through shared memory and stored with TMA
     // per 16 degrees (one box of this warp's RW rows; no CTA-wide barrier)
+#ifdef HPFEM_YPROF
+    const long long tb0 = clock64();
+#endif
     double z = 0.0;
     const int RW = 16 / EG;            // rows per warp (EG is a power of two <= 8)
     const int wr0 = (tid >> 5) * RW;   // first row of this warp
 #pragma unroll
-    for (int sg = 0; sg < CL / KCP; ++sg) {
-      if (KCP * sg < my) {
-        double* o = obuf + ((size_t)ob * NW + (tid >> 5)) * (32 * 8);  // [RW][EG][16] = 256 doubles
-        if (lane == 0) bulk_wait_read<1>();  // the store that last used this buffer has read it
+    for (int sp = 0; sp < CL / KCP; sp += SPB) {  // SPB stages share one staging buffer / fence
+      if (KCP * sp < my) {
+        double* ob0 = obuf + ((size_t)ob * NW + (tid >> 5)) * (SPB * 32 * 8);  // SPB x [RW][EG][16]
+#ifdef HPFEM_YPROF
+        t0 = clock64();
+#endif
+        if (lane == 0) bulk_wait_read<NOBUF - 1>();  // the stores that last used this buffer have read it
         __syncwarp();
+#ifdef HPFEM_YPROF
+        t_br += clock64() - t0;
+#endif
 #pragma unroll
-        for (int u = 0; u < KCP; ++u) {
-          const int c = KCP * sg + u;
-          const double zn = fma(-fb[4 * c + 2], z, fb[4 * c] * ys[c]);
-          const bool live = valid && c < mthr;
-          z = live ? zn : z;
-          const double zv = live ? zn : 0.0;
-          o[swz((r - wr0) * EG + eo, u, py)] = zv;
-          if (sg == 0 && u == 0 && live && P.z01)  // chain-first bubble (degree py): compact copy
-            P.z01[(size_t)(x.nh + kx * x.n + e_x) * (2 * y.n) + 2 * ey + py] = zn;
+        for (int h = 0; h < SPB; ++h) {
+          const int sg = sp + h;
+          if (sg < CL / KCP && KCP * sg < my) {
+            double* o = ob0 + h * 256;
+#pragma unroll
+            for (int u = 0; u < KCP; ++u) {
+              const int c = KCP * sg + u;
+              const double zn = fma(-fb[4 * c + 2], z, fb[4 * c] * ys[c]);
+              const bool live = valid && c < mthr;
+              z = live ? zn : z;
+              const double zv = live ? zn : 0.0;
+              o[swz((r - wr0) * EG + eo, u, py)] = zv;
+              if (sg == 0 && u == 0 && live && P.z01)  // chain-first bubble (degree py): compact copy
+                P.z01[(size_t)(x.nh + kx * x.n + e_x) * (2 * y.n) + 2 * ey + py] = zn;
+            }
+          }
         }
+#ifdef HPFEM_YPROF
+        t0 = clock64();
+#endif
         fence_proxy_async();
         __syncwarp();
         if (lane == 0 && wr0 < R) {
-          tma_store_4d(pi ? &mO1 : &mO0, o, 2 * KCP * sg, e0, e_x, t.kw * R + wr0);
+#pragma unroll
+          for (int h = 0; h < SPB; ++h)
+            if (sp + h < CL / KCP && KCP * (sp + h) < my)
+              tma_store_4d(pi ? &mO1 : &mO0, ob0 + h * 256, 2 * KCP * (sp + h), e0, e_x, t.kw * R + wr0);
           bulk_commit();
         }
-        ob ^= 1;
+#ifdef HPFEM_YPROF
+        t_fe += clock64() - t0;
+#endif
+        ob = ob + 1 == NOBUF ? 0 : ob + 1;
       }
     }
+#ifdef HPFEM_YPROF
+    t_bwd += clock64() - tb0;
+#endif
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#ifdef HPFEM_YPROF
+  t_all = clock64() - t_all;
+  if (lane == 0 && blockIdx.x < 2)
+    printf("yprof blk %d warp %d: all %lld  wait-first %lld  wait-other %lld  bwd %lld (wait_read %lld fence+store %lld) tiles %u\n",
+           blockIdx.x, threadIdx.x >> 5, t_all, t_w0, t_w, t_bwd, t_br, t_fe, ctt);
+#endif
 }
 /* ------------------------------------------------------------------ */
 /* precomputed stencil weights of the bubble lines (one ST_APPLY step)  */
@@ -836,7 +886,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
   A.off_h = A.off_w + round1024(wb);
   A.stage_bytes = round1024(A.off_h + hb);
   A.tx_bytes = gb + wb + hb;
-  const int obytes = 2 * NW * 256 * 8;
+  const int obytes = NOBUF * NW * SPB * 256 * 8;
   A.fac_doubles = (2 * A.EG * P.f.cfs + 15) & ~15;
   A.wb_doubles = P.wtab ? ((A.R * 6 + 15) & ~15) : 0;
   A.S = (chain_len(y.p, 0) - 1) / KCP + 1;
