@@ -65,8 +65,9 @@ def _declare(L):
     L.oracle_adi_solve.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _d, _dp, _dp, _i, _ip]
     L.oracle_apply.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _dp, _dp]
     L.oracle_load.argtypes = [_dp, _i, _i, _dp, _i, _i, _i, _dp, _dp]
+    L.oracle_unload.argtypes = [_dp, _i, _i, _dp, _i, _i, _i, _dp, _dp]
     for f in ("oracle_operator_dense", "oracle_operator_coo", "oracle_factor_dense", "oracle_solve1d",
-              "oracle_spectrum", "oracle_shifts", "oracle_plan", "oracle_adi_solve", "oracle_apply", "oracle_load"):
+              "oracle_spectrum", "oracle_shifts", "oracle_plan", "oracle_adi_solve", "oracle_apply", "oracle_load", "oracle_unload"):
         getattr(L, f).restype = _i
 
 
@@ -204,6 +205,16 @@ def load(xs, px, ys, py, bc, Fleg):
     G = np.empty((Nx, Ny))
     _check(lib().oracle_load(_ptr(xs), xs.size - 1, px, _ptr(ys), ys.size - 1, py, bc, _ptr(Fleg), _ptr(G)))
     return G
+
+
+def unload(xs, px, ys, py, bc, U):
+    """C_leg = R_x U R_y^T: piecewise-Legendre coefficients of the FEM function
+    (NEXT-1 of SURVEY 8(f); basis change of P:L392-L399 / eq. app:1 P:L1074)."""
+    xs, ys, U = _f64(xs), _f64(ys), _f64(U)
+    Lx, Ly = (px + 1) * (xs.size - 1), (py + 1) * (ys.size - 1)
+    C = np.empty((Lx, Ly))
+    _check(lib().oracle_unload(_ptr(xs), xs.size - 1, px, _ptr(ys), ys.size - 1, py, bc, _ptr(U), _ptr(C)))
+    return C
 
 
 def l2_norm_sq(xs, px, ys, py, bc, U):

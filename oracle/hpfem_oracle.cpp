@@ -882,4 +882,51 @@ int oracle_load(const double* xs, int nx, int px, const double* ys, int ny, int 
   }
 }
 
+/* Unload (NEXT-1; the coefficient map behind P:L392-L399):
+ * the piecewise-Legendre coefficients of the FEM function u = sum U_ij
+ * phi_i(x) psi_j(y),  C_leg = R_x U R_y^T, with R the same element-local
+ * basis -> Legendre change of basis as in oracle_load (hats (1 -+ t)/2,
+ * W_k = (P_k - P_{k+2})/(2k+3), eq. app:1 P:L1074) and no mass weight.
+ * U: Nx x Ny; C_leg: ((px+1) nx) x ((py+1) ny), degree-major as F_leg. */
+int oracle_unload(const double* xs, int nx, int px, const double* ys, int ny, int py, int bc, const double* U,
+                  double* Cleg) {
+  try {
+    Space sx = make_space(xs, nx, px, bc), sy = make_space(ys, ny, py, bc);
+    const std::vector<double> R_x = local_R(px), R_y = local_R(py);
+    // global sparse R as rows (Legendre index) -> (dof, value)
+    auto build = [](const Space& s, const std::vector<double>& Rl) {
+      std::vector<std::vector<std::pair<int, double>>> Z((size_t)(s.p + 1) * s.n);
+      const int nl = s.p + 1;
+      for (int e = 0; e < s.n; ++e)
+        for (int m = 0; m <= s.p; ++m)
+          for (int a = 0; a < nl; ++a) {
+            const double r = Rl[m * nl + a];
+            if (r == 0.0) continue;
+            const int g = local_to_global(s, e, a);
+            if (g < 0) continue;
+            Z[(size_t)m * s.n + e].push_back({g, r});
+          }
+      return Z;
+    };
+    auto Zx = build(sx, R_x), Zy = build(sy, R_y);
+    const int Lx = (px + 1) * nx, Ly = (py + 1) * ny, Ny = sy.N();
+    std::vector<double> T((size_t)Lx * Ny, 0.0);  // R_x U
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < Lx; ++r)
+      for (auto& gv : Zx[r])
+        for (int j = 0; j < Ny; ++j) T[(size_t)r * Ny + j] += gv.second * U[(size_t)gv.first * Ny + j];
+    // C_leg = T R_y^T
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < Lx; ++r)
+      for (int c = 0; c < Ly; ++c) {
+        double acc = 0.0;
+        for (auto& gv : Zy[c]) acc += T[(size_t)r * Ny + gv.first] * gv.second;
+        Cleg[(size_t)r * Ly + c] = acc;
+      }
+    return 0;
+  } catch (std::exception& ex) {
+    return fail(ex.what(), -1);
+  }
+}
+
 }  // extern "C"

@@ -432,6 +432,42 @@ def test_load_vs_quadrature(bc):
     assert np.abs(G - Gq).max() <= 1e-13 * np.abs(Gq).max()
 
 
+@pytest.mark.parametrize("bc", [0, 1])
+def test_unload_pointwise(bc):
+    """C_leg = R_x U R_y^T reproduces the FEM function pointwise: the
+    Legendre series with coefficients C_leg equals sum U_ij phi_i(x) psi_j(y)
+    (basis evaluated from the Jacobi definition of W_k) at random
+    points (NEXT-1 of SURVEY 8(f))."""
+    xs, px = rand_mesh(3), 6
+    ys, py = rand_mesh(2, 0, 2), 5
+    Nx, Ny = fem_ref.ndofs(xs.size - 1, px, bc), fem_ref.ndofs(ys.size - 1, py, bc)
+    U = RNG.standard_normal((Nx, Ny))
+    C = oracle.unload(xs, px, ys, py, bc, U)
+    x = np.sort(RNG.uniform(xs[0], xs[-1], 17))
+    y = np.sort(RNG.uniform(ys[0], ys[-1], 13))
+    Px, _ = fem_ref.basis_at(xs, px, bc, x)
+    Py, _ = fem_ref.basis_at(ys, py, bc, y)
+    Lx = fem_ref.legendre_basis_at(xs, px, x)
+    Ly = fem_ref.legendre_basis_at(ys, py, y)
+    u_fem = Px @ U @ Py.T
+    u_leg = Lx @ C @ Ly.T
+    assert np.abs(u_fem - u_leg).max() <= 1e-13 * np.abs(u_fem).max()
+
+
+@pytest.mark.parametrize("bc", [0, 1])
+def test_load_of_unload_is_mass(bc):
+    """load(unload(U)) = R^T M_P R U R^T M_P R = M_x U M_y (Gram matrix of the
+    basis), M from the quadrature reference."""
+    xs, px = rand_mesh(4), 5
+    ys, py = rand_mesh(3, 0, 1.5), 7
+    _, Mx = fem_ref.assemble_quad(xs, px, bc)
+    _, My = fem_ref.assemble_quad(ys, py, bc)
+    U = RNG.standard_normal((Mx.shape[0], My.shape[0]))
+    G = oracle.load(xs, px, ys, py, bc, oracle.unload(xs, px, ys, py, bc, U))
+    ref = Mx @ U @ My
+    assert np.abs(G - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
 # ------------------------------------------------- manufactured solution
 def _manufactured_error(n, p):
     """u = sin(pi x) sin(pi y) e^{x+y} on [0,1]^2 (north_star); returns the
