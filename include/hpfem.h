@@ -115,6 +115,16 @@ int hpfem_apply(hpfem_plan_t plan, const double* U, double* F, void* cuda_stream
  * element (e, f)).  G: device, N_x x N_y.  Must not overlap. */
 int hpfem_load(hpfem_plan_t plan, const double* F_leg, double* G, void* cuda_stream);
 
+/* hpfem_unload -- C_leg = R_x U R_y^T: the piecewise-Legendre coefficients
+ * of the FEM function u = sum_ij U_ij phi_i(x) psi_j(y) (the inverse basis
+ * change of the load, P:L392-L399 with the local R of eq. app:1, P:L1074;
+ * NEXT-1 of SURVEY 8(f)).  U: device N_x x N_y (the layout above); C_leg:
+ * device ((p_x+1) n_x) x ((p_y+1) n_y), degree-major / element-minor like
+ * F_leg (row m n_x + e = Legendre degree m on x-element e).  One kernel, no
+ * workspace.  EINVAL on null or overlapping buffers.  The profile kind of
+ * this call is 3 (the load/unload kind). */
+int hpfem_unload(hpfem_plan_t plan, const double* U, double* C_leg, void* cuda_stream);
+
 /* Kernel launches enqueued by the last hpfem_* device call of this plan
  * (for the bench's launch accounting). */
 int hpfem_plan_launches(hpfem_plan_t plan, long long* launches);

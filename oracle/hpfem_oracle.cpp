@@ -505,10 +505,23 @@ int shifts(double a, double b, double c, double d, double eps, int maxJ, int* Jo
   const q128 kp = 1 / alpha;
   const q128 K = pi / (2 * agm(1, kp));
   const bool symmetric = (c == -b) && (d == -a);
+  // [READING R15] exactly one interval is a single point (N = 1 in that
+  // direction): alpha = 1 and the Moebius map through (-alpha, -1, 1)
+  // degenerates.  r(z) = (z - p)/(z - q) with p (or q) at that point is
+  // exactly 0 there, so the contraction factor max|r| max|1/r| of the ADI
+  // error is 0; the other shift is taken inside its own interval
+  // (geometric mean), keeping both shifted matrices definite.
+  const bool pt_ab = (a == b), pt_cd = (c == d);
   for (int j = 1; j <= J; ++j) {
     const q128 u = (2 * j - 1) * K / (2 * (q128)J);
     const q128 dn = dn_q(u, K, kp);
-    if (symmetric) {
+    if (pt_ab && !pt_cd) {
+      P[j - 1] = a;
+      Qs[j - 1] = -(double)sqrtq(qc * qd);
+    } else if (pt_cd && !pt_ab) {
+      P[j - 1] = (double)sqrtq(qa * qb);
+      Qs[j - 1] = c;
+    } else if (symmetric) {
       // T(z) = -b/z maps (-alpha,-1,1,alpha) -> (a,b,-b,-a) since alpha = b/a
       P[j - 1] = (double)(qa / dn);
       Qs[j - 1] = (double)(-(qa / dn));

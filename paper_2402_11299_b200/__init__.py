@@ -48,6 +48,7 @@ def _load():
     L.hpfem_solve_iters.argtypes = [_vp, _vp, _vp, _i, _vp]
     L.hpfem_apply.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_load.argtypes = [_vp, _vp, _vp, _vp]
+    L.hpfem_unload.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_plan_launches.argtypes = [_vp, ctypes.POINTER(ctypes.c_longlong)]
     L.hpfem_plan_profile.argtypes = [_vp, _i]
     L.hpfem_plan_profile_read.argtypes = [_vp, _dp, ctypes.POINTER(ctypes.c_longlong), _dp]
@@ -55,7 +56,7 @@ def _load():
     L.hpfem_plan_destroy.restype = None
     L.hpfem_last_error.restype = ctypes.c_char_p
     for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
-              "hpfem_solve_iters", "hpfem_apply", "hpfem_load", "hpfem_plan_launches", "hpfem_plan_profile",
+              "hpfem_solve_iters", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
               "hpfem_plan_profile_read"):
         getattr(L, f).restype = _i
     _LIB = L
@@ -63,7 +64,7 @@ def _load():
 
 
 EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
-           "hpfem_solve_iters", "hpfem_apply", "hpfem_load", "hpfem_plan_launches", "hpfem_plan_profile",
+           "hpfem_solve_iters", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
            "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error")
 
 
@@ -151,6 +152,10 @@ def hpfem_load(plan: int, F_leg, G, stream=None):
     _check(_load().hpfem_load(plan, _ptr(F_leg), _ptr(G), _stream(stream)))
 
 
+def hpfem_unload(plan: int, U, C_leg, stream=None):
+    _check(_load().hpfem_unload(plan, _ptr(U), _ptr(C_leg), _stream(stream)))
+
+
 def hpfem_plan_launches(plan: int) -> int:
     n = ctypes.c_longlong(0)
     _check(_load().hpfem_plan_launches(plan, ctypes.byref(n)))
@@ -209,6 +214,9 @@ class Plan:
 
     def load(self, F_leg, G, stream=None):
         hpfem_load(self.handle, F_leg, G, stream)
+
+    def unload(self, U, C_leg, stream=None):
+        hpfem_unload(self.handle, U, C_leg, stream)
 
     def profile(self, capacity: int):
         hpfem_plan_profile(self.handle, capacity)

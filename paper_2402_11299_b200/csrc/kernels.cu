@@ -1107,6 +1107,62 @@ __global__ void __launch_bounds__(128) k_load2d(DirDev x, DirDev y, const double
   G[(size_t)i * y.N + j] = acc;
 }
 
+/* Unload (NEXT-1): Legendre coefficient (degree m, element e) of direction
+ * o as a combination of <= 3 dofs (R of eq. app:1): bubbles
+ * (m, e) [1/(2m+3)] and (m-2, e) [-1/(2m-1)], plus for m = 0, 1 the two hats
+ * of e ((1 -+ t)/2 = P0/2 -+ P1/2). */
+__device__ __forceinline__ void unload_sources(const DirDev& o, int r, int* d, double* w) {
+  const int n = o.n, m = r / n, e = r - m * n;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    d[q] = -1;
+    w[q] = 0.0;
+  }
+  if (m <= o.p - 2) {
+    d[0] = o.nh + m * n + e;
+    w[0] = 1.0 / (2.0 * m + 3.0);
+  }
+  if (m >= 2) {
+    d[1] = o.nh + (m - 2) * n + e;
+    w[1] = -1.0 / (2.0 * m - 1.0);
+  } else {
+    const int hl = hat_of_node(e, n, o.bc), hr = hat_of_node(e + 1, n, o.bc);
+    d[1] = hl;
+    w[1] = m == 0 ? 0.5 : -0.5;
+    d[2] = hr;
+    w[2] = 0.5;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_unload2d(DirDev x, DirDev y, const double* __restrict__ U,
+                                                   double* __restrict__ C) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  const int Ly = (y.p + 1) * y.n;
+  if (s >= Ly) return;
+  int dx[3], dy[3];
+  double wx[3], wy[3];
+  unload_sources(x, r, dx, wx);
+  unload_sources(y, s, dy, wy);
+  double acc = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (dx[a] < 0) continue;
+    double t = 0.0;
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      if (dy[b] >= 0) t += wy[b] * __ldg(U + (size_t)dx[a] * y.N + dy[b]);
+    acc += wx[a] * t;
+  }
+  C[(size_t)r * Ly + s] = acc;
+}
+
+cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, double* Cleg, cudaStream_t st) {
+  dim3 grid(((y.p + 1) * y.n + 127) / 128, (x.p + 1) * x.n);
+  k_unload2d<<<grid, 128, 0, st>>>(x, y, U, Cleg);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st) {
   dim3 grid((y.N + 127) / 128, x.N);
   k_load2d<<<grid, 128, 0, st>>>(x, y, Fleg, G);

@@ -222,10 +222,18 @@ int zolotarev(double a, double b, double c, double d, double tol, int& J, double
   const f128 T[4] = {iw[0] * sz[0] + iw[1] * sz[2], iw[0] * sz[1] + iw[1] * sz[3], iw[2] * sz[0] + iw[3] * sz[2],
                      iw[2] * sz[1] + iw[3] * sz[3]};
   auto mob = [&](f128 z) { return (T[0] * z + T[1]) / (T[2] * z + T[3]); };
+  // one-point spectrum in exactly one direction (N = 1 there): the Moebius
+  // map degenerates (al = 1); the shift at that point annihilates the error
+  // of that direction in one step, the other is any point of its interval
+  // (reading R15)
+  const bool deg_x = a == b, deg_y = c == d;
   for (int j = 1; j <= J; ++j) {
     const f128 u = (f128)(2 * j - 1) * K / (2.0Q * J);
     const f128 dn = dn128(u, K, kp);
-    if (sym) {
+    if (deg_x != deg_y) {
+      P[j - 1] = deg_x ? a : (double)sqrtq(A * B);
+      Q[j - 1] = deg_y ? c : -(double)sqrtq(C * D);
+    } else if (sym) {
       // T(z) = -b/z (al = b/a): p_j = a/dn_j, q_j = -p_j
       P[j - 1] = (double)(A / dn);
       Q[j - 1] = -P[j - 1];
@@ -696,6 +704,22 @@ int hpfem_load(hpfem_plan_t pl, const double* F_leg, double* G, void* cuda_strea
   const int e0 = prof_mark(pl, st);
   const int rc = count_launch(pl, launch_load2d(pl->dx, pl->dy, F_leg, G, st), "load");
   prof_add(pl, 3, e0, prof_mark(pl, st), (double)bl + (double)bg);
+  return rc;
+}
+
+int hpfem_unload(hpfem_plan_t pl, const double* U, double* C_leg, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !U || !C_leg) return set_err(HPFEM_EINVAL, "null argument");
+  const size_t bu = sizeof(double) * (size_t)pl->hx.N * pl->hy.N;
+  const size_t bl = sizeof(double) * (size_t)(pl->hx.p + 1) * pl->hx.n * (pl->hy.p + 1) * pl->hy.n;
+  const char* a = (const char*)U;
+  const char* b = (const char*)C_leg;
+  if (a < b + bl && b < a + bu) return set_err(HPFEM_EINVAL, "U and C_leg overlap");
+  pl->launches = 0;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int e0 = prof_mark(pl, st);
+  const int rc = count_launch(pl, launch_unload2d(pl->dx, pl->dy, U, C_leg, st), "unload");
+  prof_add(pl, 3, e0, prof_mark(pl, st), (double)bl + (double)bu);
   return rc;
 }
 

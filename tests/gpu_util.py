@@ -50,6 +50,15 @@ def gpu_load(plan, Fleg: np.ndarray) -> np.ndarray:
     return Gd.cpu().numpy()
 
 
+def gpu_unload(plan, U: np.ndarray) -> np.ndarray:
+    torch = torch_cuda()
+    Ud = torch.from_numpy(np.ascontiguousarray(U)).cuda()
+    Cd = torch.empty(((plan.px + 1) * plan.nx, (plan.py + 1) * plan.ny), dtype=torch.float64, device="cuda")
+    plan.unload(Ud, Cd)
+    torch.cuda.synchronize()
+    return Cd.cpu().numpy()
+
+
 def parity(xs, px, ys, py, bc, U, Uref):
     """(L2 relative difference, plain coefficient 2-norm relative difference)."""
     l2 = oracle.l2_rel_diff(xs, px, ys, py, bc, U, Uref)

@@ -13,7 +13,7 @@ import pytest
 
 import oracle
 import workloads as W
-from gpu_util import gpu_apply, gpu_load, gpu_plan, gpu_solve, parity, torch_cuda
+from gpu_util import gpu_apply, gpu_load, gpu_plan, gpu_solve, gpu_unload, parity, torch_cuda
 
 pytestmark = pytest.mark.gpu
 
@@ -39,6 +39,8 @@ SMALL = [
     (np.linspace(-1, 1, 6), 12, np.linspace(-1, 1, 7), 10, 10.0, 0, 1e-10),
     (rmesh(3, 0, 1, 3), 40, rmesh(2, 0, 1, 4), 70, 0.0, 0, 1e-12),  # chains > 32
     (np.linspace(0, 1, 3), 150, np.linspace(0, 1, 2), 140, 0.5, 0, 1e-8),  # chains > 64 (long path)
+    (rmesh(1, 0, 1, 5), 2, rmesh(3, 0, 2, 6), 24, 0.7, 0, 1e-10),  # N_x = 1 only: reading R15
+    (rmesh(4, 0, 1, 7), 24, rmesh(1, 0, 2, 8), 2, 0.7, 0, 1e-10),  # N_y = 1 only
 ]
 
 
@@ -118,6 +120,38 @@ def test_config_load(i):
     G = gpu_load(plan, Fleg)
     Gref = oracle.load(xs, c.px, ys, c.py, c.bc, Fleg)
     assert np.abs(G - Gref).max() <= 1e-14 * np.abs(Gref).max()
+
+
+@pytest.mark.parametrize("i", [1, 2, 3, 4])
+def test_config_unload(i):
+    """hpfem_unload (C_leg = R_x U R_y^T, NEXT-1) vs oracle_unload at full size,
+    and the identity load(unload(U)) = M_x U M_y through the CUDA path."""
+    c = W.CONFIGS[i]
+    xs, ys = c.breakpoints()
+    plan = gpu_plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
+    U = W.random_field((plan.Nx, plan.Ny), 12)
+    C = gpu_unload(plan, U)
+    Cref = oracle.unload(xs, c.px, ys, c.py, c.bc, U)
+    assert np.abs(C - Cref).max() <= 1e-14 * np.abs(Cref).max()
+    if i <= 2:
+        G = gpu_load(plan, C)
+        Mx = oracle.operator_sparse(xs, c.px, c.bc, 1)
+        My = oracle.operator_sparse(ys, c.py, c.bc, 1)
+        ref = (Mx @ (My @ U.T).T)
+        assert np.abs(G - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_unload_small_shapes():
+    """Edge shapes: p = 2 (no odd bubbles), one element, Neumann / Dirichlet."""
+    for (n, p, bc) in [(1, 2, 0), (1, 2, 1), (3, 3, 0), (2, 9, 1), (5, 4, 0)]:
+        xs = rmesh(n, seed=n + p)
+        ys = rmesh(n + 1, 0.0, 2.0, seed=p)
+        om = 1.0 if bc else 0.0
+        plan = gpu_plan(xs, p, ys, p + 1, om, bc, 1e-8)
+        U = W.random_field((plan.Nx, plan.Ny), n * 7 + p)
+        C = gpu_unload(plan, U)
+        Cref = oracle.unload(xs, p, ys, p + 1, bc, U)
+        assert np.abs(C - Cref).max() <= 1e-14 * max(np.abs(Cref).max(), 1e-300)
 
 
 @pytest.mark.parametrize("i", [1, 2, 3])

@@ -355,6 +355,26 @@ def test_adi_contraction_per_J():
     assert len(seen) >= 10
 
 
+@pytest.mark.parametrize("swap", [False, True])
+def test_adi_one_point_spectrum(swap):
+    """Reading R15: N = 1 in exactly one direction (a one-point interval, the
+    Moebius map of R5 degenerates).  The shift at that point makes the ADI
+    error factor (z - p)/(z - q) vanish there, so the FIRST iteration is
+    already the dense Kronecker solution to rounding; the
+    shifts are finite with p > 0 > q."""
+    a = (rand_mesh(1), 2)           # N = 1 (Dirichlet, one element, p = 2)
+    b = (rand_mesh(3, 0, 2), 4)     # N = 11
+    (xs, px), (ys, py) = (b, a) if swap else (a, b)
+    om, bc = 0.7, 0
+    Nx, Ny = oracle.dim(xs.size - 1, px, bc), oracle.dim(ys.size - 1, py, bc)
+    G = RNG.standard_normal((Nx, Ny))
+    Us, _, _, _, _ = _dense_sylvester(xs, px, ys, py, om, bc, G)
+    pl = oracle.plan(xs, px, ys, py, om, bc, 1e-10)
+    assert np.all(np.isfinite(pl["p"])) and np.all(pl["p"] > 0) and np.all(pl["q"] < 0)
+    U1, _ = oracle.adi_solve(xs, px, ys, py, om, bc, 1e-10, G, iters=1)
+    assert np.abs(U1 - Us).max() <= 1e-12 * np.abs(Us).max()
+
+
 def test_adi_1x1():
     """n = 1, p = 2, Dirichlet: N = 1 (no hats), gamma = 1 and the
     first iteration is exact: U = G / (2 a m) with, on the reference
