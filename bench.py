@@ -343,7 +343,8 @@ def run_ours(args, cfg):
                    "n": [cfg.nx, cfg.ny], "p": [cfg.px, cfg.py], "omega": cfg.omega,
                    "bc": "neumann" if cfg.bc else "dirichlet", "tol": cfg.tol, "mesh": cfg.mesh,
                    "step": "hpfem_load + hpfem_solve", "parallelism": f"replicas{ws}",
-                   "l2_flush": "not needed: every array (>= 2 GB at config 5) exceeds the 126 MB L2",
+                   "l2_flush": ("not needed: every array exceeds the 126 MB L2" if 8.0 * Nx * Ny > 126e6 else
+                                "none: arrays are L2-resident at this config (an L2 number)"),
                    "plan_ms": plan_ms},
         "dof_per_s": value * Nx * Ny,
         "hbm_alg_GBps": roofline["solve_alg_GBps"] * ws,
@@ -362,6 +363,103 @@ def run_ours(args, cfg):
     return 0
 
 
+def run_batched(args, cfg):
+    """--batch B > 1 (NEXT-1): B independent right-hand sides per step through
+    hpfem_load (per problem) + hpfem_solve_batched; the small configurations'
+    throughput line.  One GPU (replicas under torchrun like the default)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_11299_b200 as hp
+    import workloads as W
+
+    import numpy as np
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    stream = torch.cuda.current_stream()
+    B = args.batch
+    xs, ys = cfg.breakpoints()
+    Fleg = np.stack([W.f_leg(cfg, seed=b) for b in range(B)])
+    Fh = torch.from_numpy(Fleg).pin_memory()
+    plan = hp.Plan(xs, cfg.px, ys, cfg.py, cfg.omega, cfg.bc, cfg.tol)
+    Nx, Ny, J = plan.Nx, plan.Ny, plan.J
+    Fd = Fh.to(f"cuda:{dev}")
+    Gd = torch.empty((B, Nx, Ny), dtype=torch.float64, device=dev)
+    Ud = torch.empty_like(Gd)
+    Uh = torch.empty((B, Nx, Ny), dtype=torch.float64).pin_memory()
+
+    def step():
+        for b in range(B):
+            plan.load(Fd[b], Gd[b])
+        plan.solve_batched(Gd, Ud)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(gpu_id_for(dev)) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = plan.launches() + B  # the batched solve's kernels + one load per problem
+    t_max_s = reduce_max(start.elapsed_time(end) / 1e3, f"cuda:{dev}" if ws > 1 else None)
+    value = B * job_value(ws, args.steps, t_max_s)
+    ms_per_step = t_max_s * 1e3 / args.steps
+    e2e = None
+    if not args.no_e2e:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            Fd.copy_(Fh, non_blocking=True)
+            step()
+            Uh.copy_(Ud, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = reduce_max(e0.elapsed_time(e1) / 1e3, f"cuda:{dev}" if ws > 1 else None)
+        e2e = {"value": B * job_value(ws, args.steps, te), "unit": "solves/s",
+               "h2d_bytes_per_step": int(Fh.numel() * 8), "d2h_bytes_per_step": int(Uh.numel() * 8),
+               "ms_per_step": te * 1e3 / args.steps}
+    peak, peak_kind = measured_peak()
+    alg = 8.0 * Nx * Ny * (6 * J + 1) * B
+    achieved = alg / (ms_per_step / 1e3) / 1e9
+    resident = 3 * 8.0 * Nx * Ny * min(B, 8) < 126e6
+    line = {
+        "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{cfg.idx}:{cfg.name}", "batch": B, "N_x": Nx, "N_y": Ny, "J": J,
+                   "step": f"{B} x hpfem_load + hpfem_solve_batched", "parallelism": f"replicas{ws}",
+                   "l2_flush": ("none: the working set of the concurrent solves is L2-resident, "
+                                "so this is an L2 throughput number") if resident else "not needed"},
+        "dof_per_s": value * Nx * Ny,
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "kernel": "whole batched solve (algorithmic bytes 8 N_x N_y (6J+1) per problem)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)", "traffic": None},
+        "e2e": e2e,
+    }
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, Fleg[0], J)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -371,6 +469,7 @@ def main(argv=None):
     ap.add_argument("--config", type=int, default=5, choices=(1, 2, 3, 4, 5))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=1, help="B > 1: B right-hand sides per step (hpfem_solve_batched)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
@@ -379,6 +478,8 @@ def main(argv=None):
     cfg = W.CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.batch > 1:
+        return run_batched(args, cfg)
     return run_ours(args, cfg)
 
 

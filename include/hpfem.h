@@ -105,6 +105,20 @@ int hpfem_solve(hpfem_plan_t plan, const double* F, double* U, void* cuda_stream
  * Used for truncated-iteration parity at full size. */
 int hpfem_solve_iters(hpfem_plan_t plan, const double* F, double* U, int iters, void* cuda_stream);
 
+/* hpfem_solve_batched -- hpfem_solve for `batch` independent right-hand
+ * sides with the same plan (NEXT-1 of SURVEY 8(f): many F per plan, for the
+ * small configurations whose single solve cannot fill the GPU).
+ *   F, U: device, batch x N_x x N_y contiguous (problem b at offset b N_x N_y,
+ *   each in the layout above); U must not overlap F.
+ * The problems are spread over min(batch, HPFEM_BATCH_STREAMS (default 8))
+ * internal streams, each with its own workspace (allocated on first use and
+ * kept by the plan: 3 N_x x ld arrays per stream), forked from and joined
+ * back into cuda_stream, so the call is ordered like any other work on
+ * cuda_stream.  Each U_b is bitwise what hpfem_solve(F_b) returns.
+ * EINVAL also when profiling is on (hpfem_plan_profile records on one
+ * stream).  batch = 0 is a no-op. */
+int hpfem_solve_batched(hpfem_plan_t plan, int batch, const double* F, double* U, void* cuda_stream);
+
 /* hpfem_apply -- F = A_x U M_y + M_x U A_y (the operator of eq. adi:poisson,
  * P:L658-L664).  U, F device pointers, N_x x N_y, must not overlap. */
 int hpfem_apply(hpfem_plan_t plan, const double* U, double* F, void* cuda_stream);

@@ -49,6 +49,7 @@ def _load():
     L.hpfem_apply.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_load.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_unload.argtypes = [_vp, _vp, _vp, _vp]
+    L.hpfem_solve_batched.argtypes = [_vp, _i, _vp, _vp, _vp]
     L.hpfem_plan_launches.argtypes = [_vp, ctypes.POINTER(ctypes.c_longlong)]
     L.hpfem_plan_profile.argtypes = [_vp, _i]
     L.hpfem_plan_profile_read.argtypes = [_vp, _dp, ctypes.POINTER(ctypes.c_longlong), _dp]
@@ -56,7 +57,7 @@ def _load():
     L.hpfem_plan_destroy.restype = None
     L.hpfem_last_error.restype = ctypes.c_char_p
     for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
-              "hpfem_solve_iters", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
+              "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
               "hpfem_plan_profile_read"):
         getattr(L, f).restype = _i
     _LIB = L
@@ -64,7 +65,7 @@ def _load():
 
 
 EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
-           "hpfem_solve_iters", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
+           "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
            "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error")
 
 
@@ -144,6 +145,10 @@ def hpfem_solve_iters(plan: int, F, U, iters: int, stream=None):
     _check(_load().hpfem_solve_iters(plan, _ptr(F), _ptr(U), iters, _stream(stream)))
 
 
+def hpfem_solve_batched(plan: int, batch: int, F, U, stream=None):
+    _check(_load().hpfem_solve_batched(plan, batch, _ptr(F), _ptr(U), _stream(stream)))
+
+
 def hpfem_apply(plan: int, U, F, stream=None):
     _check(_load().hpfem_apply(plan, _ptr(U), _ptr(F), _stream(stream)))
 
@@ -214,6 +219,10 @@ class Plan:
 
     def load(self, F_leg, G, stream=None):
         hpfem_load(self.handle, F_leg, G, stream)
+
+    def solve_batched(self, F, U, stream=None):
+        """F, U: (batch, Nx, Ny) device tensors."""
+        hpfem_solve_batched(self.handle, int(F.shape[0]), F, U, stream)
 
     def unload(self, U, C_leg, stream=None):
         hpfem_unload(self.handle, U, C_leg, stream)

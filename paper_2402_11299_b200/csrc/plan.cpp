@@ -250,6 +250,19 @@ int zolotarev(double a, double b, double c, double d, double tol, int& J, double
 }  // namespace
 
 /* ======================================================================= */
+/* One set of solve buffers: the internal copy of G and the two iterates
+ * (plus the side array and the TMA tensor maps bound to them).  The plan
+ * owns one for hpfem_solve; hpfem_solve_batched adds one per stream slot. */
+struct Workspace {
+  double* Gp = nullptr;           // internal copy of G
+  double* X1 = nullptr;           // W_{j-1/2} (deferred along y), final y-solve
+  double* X2 = nullptr;           // W_j (deferred along x)
+  double* Z01 = nullptr;          // chain-first y-bubbles of X1, [row][n_y][2] (element-major layout only)
+  TmaPlan* tma = nullptr;         // TMA tensor maps over {Gp, X1, X2} (null = LDG kernels only)
+  cudaStream_t st = nullptr;      // batched solves: the slot's stream
+  cudaEvent_t done = nullptr;     // batched solves: join event
+};
+
 struct hpfem_plan_s {
   DirHost hx, hy;
   DirDev dx{}, dy{};
@@ -264,11 +277,8 @@ struct hpfem_plan_s {
   double* d_shift = nullptr;      // kap/sig arrays
   int* d_err = nullptr;
   Layout lay{};                   // internal padded layout (hpfem_internal.h)
-  double* Gp = nullptr;           // internal copy of G
-  double* X1 = nullptr;           // W_{j-1/2} (deferred along y), final y-solve
-  double* X2 = nullptr;           // W_j (deferred along x)
-  double* Z01 = nullptr;          // chain-first y-bubbles of X1, [row][n_y][2] (element-major layout only)
-  TmaPlan* tma = nullptr;         // TMA tensor maps over {Gp, X1, X2} (null = LDG kernels only)
+  Workspace ws;                   // buffers of hpfem_solve
+  std::vector<Workspace> bws;     // hpfem_solve_batched stream slots (allocated on first use)
   double* wx = nullptr;           // precomputed x-solve stencil weights, J tables
   double* wy = nullptr;           // precomputed y-solve stencil weights, J tables (table 0 unused)
   size_t wxs = 0, wys = 0;        // doubles per table
@@ -307,22 +317,54 @@ void prof_add(hpfem_plan_t pl, int kind, int e0, int e1, double bytes) {
   if (e0 >= 0 && e1 >= 0) pl->recs.push_back({kind, e0, e1, bytes});
 }
 
+void free_workspace(Workspace& w) {
+  tma_plan_destroy(w.tma);
+  cudaFree(w.Gp);
+  cudaFree(w.X1);
+  cudaFree(w.X2);
+  cudaFree(w.Z01);
+  if (w.done) cudaEventDestroy(w.done);
+  if (w.st) cudaStreamDestroy(w.st);
+  w = Workspace();
+}
+
 void free_plan(hpfem_plan_t pl) {
   if (!pl) return;
   free_events(pl);
-  tma_plan_destroy(pl->tma);
+  free_workspace(pl->ws);
+  for (Workspace& w : pl->bws) free_workspace(w);
   cudaFree(pl->fx);
   cudaFree(pl->fy);
   cudaFree(pl->d_delta);
   cudaFree(pl->d_shift);
   cudaFree(pl->d_err);
-  cudaFree(pl->Gp);
-  cudaFree(pl->X1);
-  cudaFree(pl->X2);
-  cudaFree(pl->Z01);
   cudaFree(pl->wx);
   cudaFree(pl->wy);
   delete pl;
+}
+
+/* allocate (zeroed) solve buffers and bind the TMA tensor maps to them */
+int alloc_workspace(hpfem_plan_t pl, Workspace& w, cudaStream_t st) {
+  cudaError_t ce;
+  auto fail = [&](cudaError_t e, const char* what) {
+    free_workspace(w);
+    return e == cudaErrorMemoryAllocation ? set_err(HPFEM_ENOMEM, std::string(what) + ": out of device memory")
+                                          : cuda_err(e, what);
+  };
+  const size_t bytes = sizeof(double) * ((size_t)pl->hx.N * pl->lay.ld + 64);  // +slack for bulk copies
+  for (double** b : {&w.Gp, &w.X1, &w.X2}) {
+    if ((ce = cudaMalloc(b, bytes)) != cudaSuccess) return fail(ce, "alloc workspace");
+    if ((ce = cudaMemsetAsync(*b, 0, bytes, st)) != cudaSuccess) return fail(ce, "memset workspace");
+  }
+  if (pl->use_tma) {
+    const size_t zb = sizeof(double) * ((size_t)pl->hx.N * 2 * pl->dy.n + 64);
+    if ((ce = cudaMalloc(&w.Z01, zb)) != cudaSuccess) return fail(ce, "alloc workspace");
+    if ((ce = cudaMemsetAsync(w.Z01, 0, zb, st)) != cudaSuccess) return fail(ce, "memset workspace");
+  }
+  double* const arrays[3] = {w.Gp, w.X1, w.X2};
+  w.tma = tma_plan_create(pl->dx, pl->dy, pl->lay, arrays, pl->use_tma);
+  if (pl->use_tma && !tma_supports(w.tma, 0)) return fail(cudaErrorNotSupported, "TMA tensor maps");
+  return HPFEM_OK;
 }
 
 int validate_mesh(const double* xs, int n, int p) {
@@ -425,20 +467,9 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
     pl->use_tma = !(no_tma && no_tma[0] == '1') && tma_shape_ok(pl->dx, pl->dy);
   }
   pl->lay = make_layout(pl->dy, pl->use_tma ? 1 : 0);
-  {
-    const size_t bytes = sizeof(double) * ((size_t)hx.N * pl->lay.ld + 64);  // +slack for bulk copies
-    for (double** b : {&pl->Gp, &pl->X1, &pl->X2}) {
-      if ((ce = cudaMalloc(b, bytes)) != cudaSuccess) return fail_cuda(ce, "alloc workspace");
-      if ((ce = cudaMemsetAsync(*b, 0, bytes, st)) != cudaSuccess) return fail_cuda(ce, "memset workspace");
-    }
-    if (pl->use_tma) {
-      const size_t zb = sizeof(double) * ((size_t)hx.N * 2 * pl->dy.n + 64);
-      if ((ce = cudaMalloc(&pl->Z01, zb)) != cudaSuccess) return fail_cuda(ce, "alloc workspace");
-      if ((ce = cudaMemsetAsync(pl->Z01, 0, zb, st)) != cudaSuccess) return fail_cuda(ce, "memset workspace");
-    }
-    double* const arrays[3] = {pl->Gp, pl->X1, pl->X2};
-    pl->tma = tma_plan_create(pl->dx, pl->dy, pl->lay, arrays, pl->use_tma);
-    if (pl->use_tma && !tma_supports(pl->tma, 0)) return fail_cuda(cudaErrorNotSupported, "TMA tensor maps");
+  if ((rc = alloc_workspace(pl, pl->ws, st)) != HPFEM_OK) {
+    free_plan(pl);
+    return rc;
   }
   const char* no_wtab = std::getenv("HPFEM_NO_WTAB");
   if (pl->use_tma && !(no_wtab && no_wtab[0] == '1')) {  // stencil-weight tables of every ST_APPLY half-step
@@ -506,13 +537,14 @@ bool overlap(const void* a, const void* b, size_t bytes) {
  * then the hat solve.  Algorithmic bytes per dof: read G (if used), read the
  * previous iterate (if any), write the output.
  * ia_g / ia_w: which of {Gp, X1, X2} are G and Xp (-1 = unused). */
-int run_step(hpfem_plan_t pl, StepParams P, cudaStream_t st, bool final_step, int ia_g, int ia_w) {
+int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st, bool final_step, int ia_g,
+             int ia_w) {
   const double per = 8.0 * ((P.alphaG != 0.0 ? 1 : 0) + (P.mode != ST_NONE ? 1 : 0) + 1);
   const int k0 = final_step ? 2 : 0, k1 = final_step ? 2 : 1;
   int rc;
   const int e0 = prof_mark(pl, st);
-  if (tma_supports(pl->tma, P.dir)) {
-    rc = count_launch(pl, tma_launch_step(pl->tma, P, ia_g, ia_w, st), "TMA bubble kernel");
+  if (tma_supports(w.tma, P.dir)) {
+    rc = count_launch(pl, tma_launch_step(w.tma, P, ia_g, ia_w, st), "TMA bubble kernel");
     if (rc) return rc;
     const int e1 = prof_mark(pl, st);
     prof_add(pl, k0, e0, e1, per * (double)P.o.nb * P.s.nb);
@@ -588,23 +620,13 @@ int hpfem_plan_launches(hpfem_plan_t pl, long long* launches) {
   return HPFEM_OK;
 }
 
-int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, void* cuda_stream) {
-  t_err.clear();
-  if (!pl || !F || !U) return set_err(HPFEM_EINVAL, "null argument");
-  if (iters < 0 || iters > pl->J) return set_err(HPFEM_EINVAL, "iters must lie in [0, J]");
-  const size_t bytes = sizeof(double) * (size_t)pl->hx.N * pl->hy.N;
-  if (overlap(F, U, bytes)) return set_err(HPFEM_EINVAL, "F and U overlap");
-  cudaStream_t st = (cudaStream_t)cuda_stream;
-  pl->launches = 0;
-  if (iters == 0) {  // W_0 = 0
-    cudaError_t ce = cudaMemsetAsync(U, 0, bytes, st);
-    return ce == cudaSuccess ? HPFEM_OK : cuda_err(ce, "memset");
-  }
+/* Algorithm 2 on one workspace (validated arguments, iters >= 1) */
+static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, double* U, int iters, cudaStream_t st) {
   const double hw2 = 0.5 * pl->omega * pl->omega;
   int rc;
   {
     const int e0 = prof_mark(pl, st);
-    if ((rc = count_launch(pl, launch_copyin(pl->dx, pl->dy, pl->lay, F, pl->Gp, st), "copy-in"))) return rc;
+    if ((rc = count_launch(pl, launch_copyin(pl->dx, pl->dy, pl->lay, F, w.Gp, st), "copy-in"))) return rc;
     prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);  // layout change, not algorithmic
   }
   auto base = [&](int dir) {
@@ -621,57 +643,124 @@ int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, vo
   for (int j = 0; j < iters; ++j) {
     // half-step A: W_{j-1/2} = (G - (A_x - p_j M_x) W_{j-1}) (A_y + p_j M_y)^{-1}
     StepParams A = base(1);
-    A.G = pl->Gp;
+    A.G = w.Gp;
     A.alphaG = 1.0;
     A.f = fview(pl, 1, j);
-    A.out = pl->X1;
-    A.z01 = pl->Z01;
+    A.out = w.X1;
+    A.z01 = w.Z01;
     if (j == 0) {
       A.mode = ST_NONE;  // W_0 = 0
     } else {
       const FacView prev = fview(pl, 0, j - 1);
       A.mode = ST_APPLY;
-      A.Xp = pl->X2;
+      A.Xp = w.X2;
       A.kap_a = 1.0;
       A.tau = hw2 - pl->P[j];
       A.cvL = prev.vL;
       A.cvR = prev.vR;
       if (pl->wy) A.wtab = pl->wy + pl->wys * j;
     }
-    if ((rc = run_step(pl, A, st, false, 0, j == 0 ? -1 : 2))) return rc;
+    if ((rc = run_step(pl, w, A, st, false, 0, j == 0 ? -1 : 2))) return rc;
     // half-step B: W_j = (A_x - q_j M_x)^{-1} (G - W_{j-1/2} (A_y + q_j M_y))
     StepParams B = base(0);
-    B.G = pl->Gp;
+    B.G = w.Gp;
     B.alphaG = 1.0;
     B.f = fview(pl, 0, j);
-    B.out = pl->X2;
+    B.out = w.X2;
     B.mode = ST_APPLY;
-    B.Xp = pl->X1;
-    B.z01p = pl->Z01;
+    B.Xp = w.X1;
+    B.z01p = w.Z01;
     B.kap_a = 1.0;
     B.tau = hw2 + pl->Q[j];
     B.cvL = A.f.vL;
     B.cvR = A.f.vR;
     if (pl->wx) B.wtab = pl->wx + pl->wxs * j;
-    if ((rc = run_step(pl, B, st, false, 0, 1))) return rc;
+    if ((rc = run_step(pl, w, B, st, false, 0, 1))) return rc;
   }
   // RETURN W_J C^{-1}: y-solves with the mass factor, then materialise U
   StepParams Fin = base(1);
   Fin.G = nullptr;
   Fin.alphaG = 0.0;
   Fin.f = fview(pl, 1, pl->J);
-  Fin.out = pl->X1;
-  Fin.z01 = pl->Z01;
+  Fin.out = w.X1;
+  Fin.z01 = w.Z01;
   Fin.mode = ST_CORR;
-  Fin.Xp = pl->X2;
+  Fin.Xp = w.X2;
   const FacView last = fview(pl, 0, iters - 1);
   Fin.cvL = last.vL;
   Fin.cvR = last.vR;
-  if ((rc = run_step(pl, Fin, st, true, -1, 2))) return rc;
+  if ((rc = run_step(pl, w, Fin, st, true, -1, 2))) return rc;
   const int e0 = prof_mark(pl, st);
-  rc = count_launch(pl, launch_finalize(pl->dx, pl->dy, pl->lay, Fin.f.vL, Fin.f.vR, pl->X1, U, st), "finalize");
+  rc = count_launch(pl, launch_finalize(pl->dx, pl->dy, pl->lay, Fin.f.vL, Fin.f.vR, w.X1, U, st), "finalize");
   prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);
   return rc;
+}
+
+
+int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !F || !U) return set_err(HPFEM_EINVAL, "null argument");
+  if (iters < 0 || iters > pl->J) return set_err(HPFEM_EINVAL, "iters must lie in [0, J]");
+  const size_t bytes = sizeof(double) * (size_t)pl->hx.N * pl->hy.N;
+  if (overlap(F, U, bytes)) return set_err(HPFEM_EINVAL, "F and U overlap");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  pl->launches = 0;
+  if (iters == 0) {  // W_0 = 0
+    cudaError_t ce = cudaMemsetAsync(U, 0, bytes, st);
+    return ce == cudaSuccess ? HPFEM_OK : cuda_err(ce, "memset");
+  }
+  return solve_core(pl, pl->ws, F, U, iters, st);
+}
+
+int hpfem_solve_batched(hpfem_plan_t pl, int batch, const double* F, double* U, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !F || !U) return set_err(HPFEM_EINVAL, "null argument");
+  if (batch < 0) return set_err(HPFEM_EINVAL, "batch < 0");
+  const size_t nn = (size_t)pl->hx.N * pl->hy.N;
+  if (overlap(F, U, sizeof(double) * nn * (size_t)batch)) return set_err(HPFEM_EINVAL, "F and U overlap");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  pl->launches = 0;
+  if (batch == 0) return HPFEM_OK;
+  if (!pl->ev.empty()) return set_err(HPFEM_EINVAL, "profiling is on: batched solves run on several streams");
+  int slots = batch;
+  {
+    const char* v = std::getenv("HPFEM_BATCH_STREAMS");
+    const int cap = v && *v ? std::atoi(v) : 8;
+    if (slots > cap) slots = cap;
+    if (slots < 1) slots = 1;
+  }
+  cudaError_t ce;
+  while ((int)pl->bws.size() < slots) {  // stream slots, each with its own buffers
+    Workspace w;
+    int rc = alloc_workspace(pl, w, st);
+    if (rc != HPFEM_OK) return rc;
+    if ((ce = cudaStreamCreateWithFlags(&w.st, cudaStreamNonBlocking)) != cudaSuccess ||
+        (ce = cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming)) != cudaSuccess) {
+      free_workspace(w);
+      return cuda_err(ce, "batch stream");
+    }
+    pl->bws.push_back(w);
+  }
+  // fork: every slot stream waits for the work already queued on st
+  cudaEvent_t fork = pl->bws[0].done;
+  if ((ce = cudaEventRecord(fork, st)) != cudaSuccess) return cuda_err(ce, "fork");
+  for (int k = 0; k < slots; ++k)
+    if ((ce = cudaStreamWaitEvent(pl->bws[k].st, fork, 0)) != cudaSuccess) return cuda_err(ce, "fork");
+  long long total = 0;
+  for (int b = 0; b < batch; ++b) {
+    const Workspace& w = pl->bws[b % slots];
+    pl->launches = 0;
+    const int rc = solve_core(pl, w, F + (size_t)b * nn, U + (size_t)b * nn, pl->J, w.st);
+    total += pl->launches;
+    if (rc != HPFEM_OK) return rc;
+  }
+  pl->launches = total;
+  // join
+  for (int k = 0; k < slots; ++k) {
+    if ((ce = cudaEventRecord(pl->bws[k].done, pl->bws[k].st)) != cudaSuccess) return cuda_err(ce, "join");
+    if ((ce = cudaStreamWaitEvent(st, pl->bws[k].done, 0)) != cudaSuccess) return cuda_err(ce, "join");
+  }
+  return HPFEM_OK;
 }
 
 int hpfem_solve(hpfem_plan_t pl, const double* F, double* U, void* cuda_stream) {

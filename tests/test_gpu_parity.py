@@ -211,6 +211,29 @@ def test_config5_full_solve():
     assert l2 <= tol
 
 
+@pytest.mark.parametrize("i", [1, 2])
+def test_batched_bitwise(i):
+    """hpfem_solve_batched (NEXT-1): every problem of the batch is bitwise the
+    single-RHS hpfem_solve, and the batch matches the oracle per problem."""
+    torch = torch_cuda()
+    c = W.CONFIGS[i]
+    xs, ys = c.breakpoints()
+    plan = gpu_plan(xs, c.px, ys, c.py, c.omega, c.bc, c.tol)
+    B = 11  # more problems than stream slots (8): slots are reused
+    Gs = np.stack([W.random_field((plan.Nx, plan.Ny), 100 + b) for b in range(B)])
+    Fd = torch.from_numpy(Gs).cuda()
+    Ud = torch.full_like(Fd, float("nan"))
+    plan.solve_batched(Fd, Ud)
+    torch.cuda.synchronize()
+    Ub = Ud.cpu().numpy()
+    for b in (0, 5, B - 1):
+        U1 = gpu_solve(plan, Gs[b])
+        assert np.array_equal(U1, Ub[b])
+    Uref, _ = oracle.adi_solve(xs, c.px, ys, c.py, c.omega, c.bc, c.tol, Gs[3])
+    l2, _ = parity(xs, c.px, ys, c.py, c.bc, Ub[3], Uref)
+    assert l2 <= L2_TOL
+
+
 def test_iters_zero_and_zero_rhs():
     xs, px, ys, py, om, bc, tol = SMALL[4]
     plan = gpu_plan(xs, px, ys, py, om, bc, tol)
