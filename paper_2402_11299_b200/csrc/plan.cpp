@@ -261,6 +261,8 @@ struct Workspace {
   TmaPlan* tma = nullptr;         // TMA tensor maps over {Gp, X1, X2} (null = LDG kernels only)
   cudaStream_t st = nullptr;      // batched solves: the slot's stream
   cudaEvent_t done = nullptr;     // batched solves: join event
+  cudaStream_t hs = nullptr;      // side stream: hat lines concurrent with the TMA bubble kernel
+  cudaEvent_t hfork = nullptr, hjoin = nullptr;
 };
 
 struct hpfem_plan_s {
@@ -325,6 +327,9 @@ void free_workspace(Workspace& w) {
   cudaFree(w.Z01);
   if (w.done) cudaEventDestroy(w.done);
   if (w.st) cudaStreamDestroy(w.st);
+  if (w.hfork) cudaEventDestroy(w.hfork);
+  if (w.hjoin) cudaEventDestroy(w.hjoin);
+  if (w.hs) cudaStreamDestroy(w.hs);
   w = Workspace();
 }
 
@@ -364,6 +369,12 @@ int alloc_workspace(hpfem_plan_t pl, Workspace& w, cudaStream_t st) {
   double* const arrays[3] = {w.Gp, w.X1, w.X2};
   w.tma = tma_plan_create(pl->dx, pl->dy, pl->lay, arrays, pl->use_tma);
   if (pl->use_tma && !tma_supports(w.tma, 0)) return fail(cudaErrorNotSupported, "TMA tensor maps");
+  if (pl->use_tma) {
+    if ((ce = cudaStreamCreateWithFlags(&w.hs, cudaStreamNonBlocking)) != cudaSuccess ||
+        (ce = cudaEventCreateWithFlags(&w.hfork, cudaEventDisableTiming)) != cudaSuccess ||
+        (ce = cudaEventCreateWithFlags(&w.hjoin, cudaEventDisableTiming)) != cudaSuccess)
+      return fail(ce, "side stream");
+  }
   return HPFEM_OK;
 }
 
@@ -543,7 +554,30 @@ int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st,
   const int k0 = final_step ? 2 : 0, k1 = final_step ? 2 : 1;
   int rc;
   const int e0 = prof_mark(pl, st);
-  if (tma_supports(w.tma, P.dir)) {
+  // Concurrent hat lines: the persistent TMA grid leaves `spare` SMs to the
+  // hat-line kernel on the side stream (serial when profiling, so that the
+  // per-kind times stay attributable).  HPFEM_HAT_SMS sets `spare` (0 = serial).
+  static int spare_env = -1;
+  if (spare_env < 0) {
+    const char* v = std::getenv("HPFEM_HAT_SMS");
+    spare_env = v && *v ? std::atoi(v) : 4;
+  }
+  const char* old_hl = std::getenv("HPFEM_LDG_HATLINES");
+  const bool ldg_hl = old_hl && old_hl[0] == '1';
+  if (tma_supports(w.tma, P.dir) && P.o.nh > 0 && spare_env > 0 && e0 < 0 && pl->ev.empty() && w.hs && !ldg_hl) {
+    StepParams H = P;
+    H.lp_begin = P.dir == 0 ? 0 : P.o.nb;
+    H.lp_count = P.o.nh;
+    cudaError_t ce;
+    if ((ce = cudaEventRecord(w.hfork, st)) != cudaSuccess) return cuda_err(ce, "fork");
+    rc = count_launch(pl, tma_launch_step(w.tma, P, ia_g, ia_w, st, spare_env), "TMA bubble kernel");
+    if (rc) return rc;
+    if ((ce = cudaStreamWaitEvent(w.hs, w.hfork, 0)) != cudaSuccess) return cuda_err(ce, "fork");
+    rc = count_launch(pl, launch_hat_lines(H, w.hs), "hat-line kernel");
+    if (rc) return rc;
+    if ((ce = cudaEventRecord(w.hjoin, w.hs)) != cudaSuccess) return cuda_err(ce, "join");
+    if ((ce = cudaStreamWaitEvent(st, w.hjoin, 0)) != cudaSuccess) return cuda_err(ce, "join");
+  } else if (tma_supports(w.tma, P.dir)) {
     rc = count_launch(pl, tma_launch_step(w.tma, P, ia_g, ia_w, st), "TMA bubble kernel");
     if (rc) return rc;
     const int e1 = prof_mark(pl, st);
@@ -553,9 +587,7 @@ int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st,
     H.lp_begin = P.dir == 0 ? 0 : P.o.nb;
     H.lp_count = P.o.nh;
     if (H.lp_count > 0) {
-      const char* old_hl = std::getenv("HPFEM_LDG_HATLINES");
-      rc = count_launch(pl, (old_hl && old_hl[0] == '1') ? launch_step_bubbles(H, st) : launch_hat_lines(H, st),
-                        "hat-line kernel");
+      rc = count_launch(pl, ldg_hl ? launch_step_bubbles(H, st) : launch_hat_lines(H, st), "hat-line kernel");
       if (rc) return rc;
       prof_add(pl, k1, e1, prof_mark(pl, st), per * (double)P.o.nh * P.s.nb);
     }

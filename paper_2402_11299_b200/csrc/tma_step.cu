@@ -828,7 +828,9 @@ static int round1024(int b) { return (b + 1023) & ~1023; }
 
 /* Launch the bubble-line part of one half-step.  ia_g / ia_w: indices of the
  * G and Xp arrays among (Gp, X1, X2) (-1 when unused). */
-cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int ia_w, cudaStream_t st) {
+cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int ia_w, cudaStream_t st,
+                            int spare_sms) {
+  const int sms = T->sms - spare_sms > 1 ? T->sms - spare_sms : 1;
   TmaStepArgs A;
   std::memset(&A, 0, sizeof(A));
   A.P = P;
@@ -865,7 +867,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
     A.fG = make_fdiv(ngroups);
     A.fT = make_fdiv(x.n);
     const size_t smem = (size_t)A.bar_off + 2 * A.nstages * sizeof(uint64_t);
-    const int grid = A.ntiles < T->sms ? A.ntiles : T->sms;
+    const int grid = A.ntiles < sms ? A.ntiles : sms;
     const int cl = chain_len(x.p, 0);
     const CUtensorMap* g = T->xv[gi];
     const CUtensorMap* w = T->xv[wi];
@@ -906,7 +908,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
   A.fG = make_fdiv(ngroups);
   A.fT = make_fdiv(A.nwt);
   const size_t smem = (size_t)A.bar_off + 2 * A.nstages * sizeof(uint64_t);
-  const int grid = A.ntiles < T->sms ? A.ntiles : T->sms;
+  const int grid = A.ntiles < sms ? A.ntiles : sms;
   const int cl = chain_len(y.p, 0);
   switch (P.mode) {
     case ST_NONE: return dispatch_y<ST_NONE>(cl, A, T, gi, wi, grid, smem, st);

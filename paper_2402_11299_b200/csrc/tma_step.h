@@ -30,8 +30,10 @@ size_t tma_wtab_doubles(const DirDev& x, const DirDev& y, const Layout& L, int d
 cudaError_t tma_build_wtab(const DirDev& x, const DirDev& y, const Layout& L, int dir, double kap, double tau,
                            const double* cvL, const double* cvR, double* wtab, cudaStream_t st);
 
-/* bubble lines of one half-step; ia_g / ia_w index {Gp, X1, X2} (-1 = unused) */
-cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int ia_w, cudaStream_t st);
+/* bubble lines of one half-step; ia_g / ia_w index {Gp, X1, X2} (-1 = unused);
+ * the persistent grid leaves `spare_sms` SMs free for concurrent work */
+cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int ia_w, cudaStream_t st,
+                            int spare_sms = 0);
 
 }  // namespace hpfem
 
