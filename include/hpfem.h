@@ -139,6 +139,25 @@ int hpfem_load(hpfem_plan_t plan, const double* F_leg, double* G, void* cuda_str
  * this call is 3 (the load/unload kind). */
 int hpfem_unload(hpfem_plan_t plan, const double* U, double* C_leg, void* cuda_stream);
 
+/*
+ * 1D solver workload (NEXT-2 of SURVEY 8(f); the paper's Fig. 1):
+ * batched solves of the 1D screened Poisson discretisation
+ *        (K + w^2 M) u = f      (Dirichlet basis Q or Neumann C)
+ * with the reverse Cholesky factor of Algorithm 1 in static-
+ * condensation form (one CTA per right-hand side).
+ *   hpfem_plan1d: breakpoints xs[0..n] (host, strictly increasing), degree
+ *     p >= 2, bc, omega (Neumann needs omega != 0); factors on the device and
+ *     synchronises cuda_stream once.  ENOTPD on a non-positive pivot.
+ *   hpfem_solve1d: F, U device, nrhs x N row-major (N from hpfem_plan1d_info,
+ *     dofs ordered as the 2D arrays' rows: hats, then degree-major bubbles);
+ *     U must not overlap F.
+ */
+typedef struct hpfem_plan1d_s* hpfem_plan1d_t;
+int hpfem_plan1d(const double* xs, int n, int p, int bc, double omega, void* cuda_stream, hpfem_plan1d_t* out);
+int hpfem_plan1d_info(hpfem_plan1d_t plan, int* N);
+int hpfem_solve1d(hpfem_plan1d_t plan, int nrhs, const double* F, double* U, void* cuda_stream);
+void hpfem_plan1d_destroy(hpfem_plan1d_t plan);
+
 /* Kernel launches enqueued by the last hpfem_* device call of this plan
  * (for the bench's launch accounting). */
 int hpfem_plan_launches(hpfem_plan_t plan, long long* launches);

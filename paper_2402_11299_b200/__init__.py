@@ -50,6 +50,10 @@ def _load():
     L.hpfem_load.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_unload.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_solve_batched.argtypes = [_vp, _i, _vp, _vp, _vp]
+    L.hpfem_plan1d.argtypes = [_dp, _i, _i, _i, _d, _vp, ctypes.POINTER(_vp)]
+    L.hpfem_plan1d_info.argtypes = [_vp, ctypes.POINTER(_i)]
+    L.hpfem_solve1d.argtypes = [_vp, _i, _vp, _vp, _vp]
+    L.hpfem_plan1d_destroy.argtypes = [_vp]
     L.hpfem_plan_launches.argtypes = [_vp, ctypes.POINTER(ctypes.c_longlong)]
     L.hpfem_plan_profile.argtypes = [_vp, _i]
     L.hpfem_plan_profile_read.argtypes = [_vp, _dp, ctypes.POINTER(ctypes.c_longlong), _dp]
@@ -58,7 +62,7 @@ def _load():
     L.hpfem_last_error.restype = ctypes.c_char_p
     for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
               "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
-              "hpfem_plan_profile_read"):
+              "hpfem_plan_profile_read", "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d"):
         getattr(L, f).restype = _i
     _LIB = L
     return L
@@ -66,7 +70,8 @@ def _load():
 
 EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
            "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
-           "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error")
+           "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error",
+           "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_plan1d_destroy")
 
 
 class HpfemError(RuntimeError):
@@ -147,6 +152,52 @@ def hpfem_solve_iters(plan: int, F, U, iters: int, stream=None):
 
 def hpfem_solve_batched(plan: int, batch: int, F, U, stream=None):
     _check(_load().hpfem_solve_batched(plan, batch, _ptr(F), _ptr(U), _stream(stream)))
+
+
+def hpfem_plan1d(xs, p: int, bc: int, omega: float, stream=None) -> int:
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    out = _vp()
+    _check(_load().hpfem_plan1d(xs.ctypes.data_as(_dp), xs.size - 1, p, bc, omega, _stream(stream), ctypes.byref(out)))
+    return out.value
+
+
+def hpfem_plan1d_info(plan: int) -> int:
+    N = _i()
+    _check(_load().hpfem_plan1d_info(plan, ctypes.byref(N)))
+    return N.value
+
+
+def hpfem_solve1d(plan: int, nrhs: int, F, U, stream=None):
+    _check(_load().hpfem_solve1d(plan, nrhs, _ptr(F), _ptr(U), _stream(stream)))
+
+
+def hpfem_plan1d_destroy(plan: int):
+    if plan:
+        _load().hpfem_plan1d_destroy(plan)
+
+
+class Plan1D:
+    """Batched 1D screened-Poisson solves (K + w^2 M) u = f (the paper's Fig. 1)."""
+
+    def __init__(self, xs, p, bc, omega, stream=None):
+        self.handle = hpfem_plan1d(xs, p, bc, omega, stream)
+        self.N = hpfem_plan1d_info(self.handle)
+
+    def solve(self, F, U, stream=None):
+        """F, U: (nrhs, N) or (N,) device tensors."""
+        nrhs = 1 if F.dim() == 1 else int(F.shape[0])
+        hpfem_solve1d(self.handle, nrhs, F, U, stream)
+
+    def close(self):
+        hpfem_plan1d_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.close()
+        except Exception:
+            pass
 
 
 def hpfem_apply(plan: int, U, F, stream=None):

@@ -154,6 +154,8 @@ cudaError_t launch_finalize(const DirDev& x, const DirDev& y, const Layout& L, c
 cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const double* U, double* F,
                            cudaStream_t st);
 cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st);
+cudaError_t launch_solve1d(const DirDev& d, const FacView& f, int nrhs, const double* F, double* U,
+                           cudaStream_t st);  // solve1d.cu
 cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, double* Cleg, cudaStream_t st);
 
 }  // namespace hpfem

@@ -844,6 +844,99 @@ int hpfem_unload(hpfem_plan_t pl, const double* U, double* C_leg, void* cuda_str
   return rc;
 }
 
+/* ---------------- 1D solver workload (NEXT-2, the paper's Fig. 1) ---------------- */
+}  // extern "C"
+
+struct hpfem_plan1d_s {
+  DirHost h;
+  DirDev d{};
+  double omega = 0;
+  double* d_delta = nullptr;
+  double* d_ks = nullptr;  // kap, sig
+  double* fac = nullptr;
+  int* d_err = nullptr;
+};
+
+static void free_plan1d(hpfem_plan1d_t pl) {
+  if (!pl) return;
+  cudaFree(pl->d_delta);
+  cudaFree(pl->d_ks);
+  cudaFree(pl->fac);
+  cudaFree(pl->d_err);
+  delete pl;
+}
+
+extern "C" {
+
+int hpfem_plan1d(const double* xs, int n, int p, int bc, double omega, void* cuda_stream, hpfem_plan1d_t* out) {
+  t_err.clear();
+  if (!out) return set_err(HPFEM_EINVAL, "null out");
+  *out = nullptr;
+  int rc;
+  if ((rc = validate_mesh(xs, n, p)) != HPFEM_OK) return rc;
+  if (bc != HPFEM_BC_DIRICHLET && bc != HPFEM_BC_NEUMANN) return set_err(HPFEM_EINVAL, "bad bc");
+  if (!std::isfinite(omega)) return set_err(HPFEM_EINVAL, "omega not finite");
+  if (bc == HPFEM_BC_NEUMANN && omega == 0.0) return set_err(HPFEM_EINVAL, "Neumann requires omega != 0");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(HPFEM_ECUDA, "no CUDA device (no CPU fallback)");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  hpfem_plan1d_t pl = new hpfem_plan1d_s();
+  pl->h = make_dir(xs, n, p, bc);
+  pl->omega = omega;
+  cudaError_t ce;
+  auto fail = [&](cudaError_t e, const char* w) {
+    free_plan1d(pl);
+    return e == cudaErrorMemoryAllocation ? set_err(HPFEM_ENOMEM, std::string(w) + ": out of device memory")
+                                          : cuda_err(e, w);
+  };
+  if ((ce = cudaMalloc(&pl->d_delta, sizeof(double) * n)) != cudaSuccess) return fail(ce, "alloc");
+  if ((ce = cudaMemcpyAsync(pl->d_delta, pl->h.delta.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st)) !=
+      cudaSuccess)
+    return fail(ce, "copy");
+  DirDev& d = pl->d;
+  d.n = n; d.p = p; d.bc = bc; d.nh = pl->h.nh; d.N = pl->h.N; d.nb = pl->h.nb; d.delta = pl->d_delta;
+  const double ks[2] = {1.0, omega * omega};  // K + w^2 M
+  if ((ce = cudaMalloc(&pl->d_ks, sizeof(ks))) != cudaSuccess) return fail(ce, "alloc");
+  if ((ce = cudaMemcpyAsync(pl->d_ks, ks, sizeof(ks), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return fail(ce, "copy");
+  const size_t stride = fac_stride(d);
+  if ((ce = cudaMalloc(&pl->fac, sizeof(double) * stride)) != cudaSuccess) return fail(ce, "alloc");
+  if ((ce = cudaMemsetAsync(pl->fac, 0, sizeof(double) * stride, st)) != cudaSuccess) return fail(ce, "memset");
+  if ((ce = cudaMalloc(&pl->d_err, sizeof(int) * 4)) != cudaSuccess) return fail(ce, "alloc");
+  if ((ce = cudaMemsetAsync(pl->d_err, 0, sizeof(int) * 4, st)) != cudaSuccess) return fail(ce, "memset");
+  if ((ce = launch_factor(d, pl->d_ks, pl->d_ks + 1, 1, pl->fac, stride, pl->d_err, st)) != cudaSuccess)
+    return fail(ce, "factor");
+  int herr[4];
+  if ((ce = cudaMemcpyAsync(herr, pl->d_err, sizeof(herr), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return fail(ce, "copy err");
+  if ((ce = cudaStreamSynchronize(st)) != cudaSuccess) return fail(ce, "sync");
+  if (herr[0]) {
+    free_plan1d(pl);
+    return set_err(HPFEM_ENOTPD, "non-positive pivot in the 1D factorisation");
+  }
+  *out = pl;
+  return HPFEM_OK;
+}
+
+int hpfem_plan1d_info(hpfem_plan1d_t pl, int* N) {
+  if (!pl) return set_err(HPFEM_EINVAL, "null plan");
+  if (N) *N = pl->h.N;
+  return HPFEM_OK;
+}
+
+int hpfem_solve1d(hpfem_plan1d_t pl, int nrhs, const double* F, double* U, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !F || !U) return set_err(HPFEM_EINVAL, "null argument");
+  if (nrhs < 0) return set_err(HPFEM_EINVAL, "nrhs < 0");
+  if (overlap(F, U, sizeof(double) * (size_t)pl->h.N * nrhs)) return set_err(HPFEM_EINVAL, "F and U overlap");
+  const FacView f = fac_view(pl->d, pl->fac, 1.0, pl->omega * pl->omega);
+  const cudaError_t ce = launch_solve1d(pl->d, f, nrhs, F, U, (cudaStream_t)cuda_stream);
+  return ce == cudaSuccess ? HPFEM_OK : cuda_err(ce, "solve1d");
+}
+
+void hpfem_plan1d_destroy(hpfem_plan1d_t pl) { free_plan1d(pl); }
+
 int hpfem_plan_profile(hpfem_plan_t pl, int capacity) {
   if (!pl || capacity < 0) return set_err(HPFEM_EINVAL, "bad argument");
   free_events(pl);

@@ -1,2 +1,2 @@
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>gpurun_out/b39.err | tail -1 > gpurun_out/b39.json; python -c "import json;d=json.loads(open('gpurun_out/b39.json').read());print(d['value'], d['ms_per_step'], d['e2e'], d['clocks'])"
-timeout 300 python bench.py --config 3 --steps 20 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys;d=json.loads(sys.stdin.read());print('cfg3', d['value'], d['e2e']['value'])"
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "solve1d" 2>&1 | tail -3
+timeout 300 python scripts/bench_1d.py > gpurun_out/fig1_1d.jsonl 2>&1; echo bench1d rc=$?; cat gpurun_out/fig1_1d.jsonl

@@ -273,3 +273,38 @@ def test_solve_plan_reuse_and_linearity():
     U3 = gpu_solve(plan, 2 * G1 - 3 * G2)
     assert np.abs(U3 - (2 * U1 - 3 * U2)).max() <= 1e-11 * np.abs(U3).max()
     assert np.array_equal(gpu_solve(plan, G1), U1)  # deterministic
+
+
+# ---------------------------------------------------------------- 1D solves
+CASES_1D = [
+    # (xs, p, bc, omega)
+    (np.array([0.0, 1.0]), 2, 0, 1.0),            # N = 1
+    (np.array([0.0, 1.0]), 7, 1, 1.0),            # one element, Neumann: 2 hats
+    (np.linspace(-1, 1, 9), 8, 0, 1.0),           # Fig. 1 shape (Dirichlet, w = 1)
+    (rmesh(17, 0, 1, 21), 33, 1, 0.5),            # odd p, Neumann
+    (W.graded_mesh(0, 1, 24, 0.7), 16, 0, 3.0),   # graded
+    (np.linspace(0, 1, 301), 3, 0, 1.0),          # many elements: long hat system
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES_1D)))
+def test_solve1d_vs_oracle(case):
+    """hpfem_solve1d (NEXT-2, Fig. 1 workload): (K + w^2 M)^{-1} F for a batch
+    of right-hand sides vs the oracle's Alg. 1 + Cor. 4.3 solve."""
+    import paper_2402_11299_b200 as hp
+
+    torch = torch_cuda()
+    xs, p, bc, om = CASES_1D[case]
+    pl = hp.Plan1D(xs, p, bc, om)
+    nrhs = 5
+    F = np.random.default_rng(case).standard_normal((nrhs, pl.N))
+    Fd = torch.from_numpy(F).cuda()
+    Ud = torch.empty_like(Fd)
+    pl.solve(Fd, Ud)
+    torch.cuda.synchronize()
+    U = Ud.cpu().numpy()
+    Uref = oracle.solve1d(xs, p, bc, 1.0, om * om, F)
+    err = np.linalg.norm(U - Uref) / np.linalg.norm(Uref)
+    print(f"1d case {case}: N={pl.N} rel err {err:.2e}")
+    assert err <= 1e-11
+    pl.close()
