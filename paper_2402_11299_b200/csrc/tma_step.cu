@@ -154,12 +154,14 @@ __device__ __forceinline__ int swz(int rho, int u, int py) { return rho * 16 + (
  * read a stage of tile t-1, i.e. after every warp has finished tile t-2,
  * the last user of that buffer. */
 __device__ __forceinline__ bool release_is_last(uint32_t* cnt, int slot) {
-  __threadfence_block();
-  const uint32_t old = atomicAdd(&cnt[slot], 1u);
+  // acq_rel atomic: this warp's reads of the slot happen-before the last
+  // releaser's refill; the reset of the counter is published by that warp's
+  // mbarrier.arrive.expect_tx (release) before any consumer can bump it again
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(su32(&cnt[slot])) : "memory");
   if (old != NW - 1) return false;
   cnt[slot] = 0;
-  __threadfence_block();
-  fence_proxy_async();
+  fence_proxy_async();  // generic-proxy reads of the slot before the async-proxy (TMA) overwrite
   return true;
 }
 
