@@ -95,6 +95,17 @@ def threads():
     return lib().oracle_threads()
 
 
+def bc2d(bx, by):
+    """2D boundary code of per-direction 1D codes (0 Dirichlet, 1 Neumann,
+    2 Dirichlet-left / Neumann-right, 3 Neumann-left / Dirichlet-right);
+    a plain 0..3 means the same code in both directions."""
+    return bx if bx == by else 16 + bx + 4 * by
+
+
+def split_bc(bc):
+    return (bc, bc) if bc < 16 else ((bc - 16) & 3, ((bc - 16) >> 2) & 3)
+
+
 def dim(n, p, bc):
     return lib().oracle_dim(n, p, bc)
 
@@ -201,7 +212,8 @@ def apply(xs, px, ys, py, omega, bc, U):
 def load(xs, px, ys, py, bc, Fleg):
     """G = R_x^T M_P,x F_leg M_P,y R_y."""
     xs, ys, Fleg = _f64(xs), _f64(ys), _f64(Fleg)
-    Nx, Ny = dim(xs.size - 1, px, bc), dim(ys.size - 1, py, bc)
+    bx, by = split_bc(bc)
+    Nx, Ny = dim(xs.size - 1, px, bx), dim(ys.size - 1, py, by)
     G = np.empty((Nx, Ny))
     _check(lib().oracle_load(_ptr(xs), xs.size - 1, px, _ptr(ys), ys.size - 1, py, bc, _ptr(Fleg), _ptr(G)))
     return G
@@ -221,8 +233,9 @@ def l2_norm_sq(xs, px, ys, py, bc, U):
     """||u||^2_{L2} of the FEM function with coefficients U: tr(U^T M_x U M_y)
     = ||V U L^T||_F^2 for M_x = V^T V, M_y = L^T L (the Lemma 5.1 norm,
     P:L733).  Used as the parity norm (reading R12)."""
-    Mx = operator_sparse(xs, px, bc, 1)
-    My = operator_sparse(ys, py, bc, 1)
+    bx, by = split_bc(bc)
+    Mx = operator_sparse(xs, px, bx, 1)
+    My = operator_sparse(ys, py, by, 1)
     U = _f64(U)
     A = Mx @ U
     B = (My @ U.T).T

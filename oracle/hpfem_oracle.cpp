@@ -52,18 +52,22 @@ namespace {
 struct Space {
   int n = 0;               // elements
   int p = 0;               // max degree per element (bubbles W_0..W_{p-2})
-  int bc = 0;              // 0 = zero Dirichlet (basis Q), 1 = zero Neumann (basis C)
+  int bc = 0;              // 0 = zero Dirichlet (basis Q), 1 = zero Neumann (basis C),
+                           // 2 = Dirichlet left / Neumann right, 3 = Neumann left / Dirichlet right
+                           // (mixed: the hat keep/drop mask of P:L430-L435, NEXT-1 of SURVEY 8(f))
   std::vector<double> x;   // breakpoints x_0 < ... < x_n
 
-  // number of hat functions kept: Q drops h_0 and h_n, C keeps all
-  int nh() const { return bc == 0 ? n - 1 : n + 1; }
-  // N = p n - 1 (Dirichlet) / p n + 1 (Neumann)
+  // a Dirichlet end drops its boundary hat (Q drops h_0 and h_n; C keeps all)
+  bool drop_left() const { return bc == 0 || bc == 2; }
+  bool drop_right() const { return bc == 0 || bc == 3; }
+  int nh() const { return n + 1 - (drop_left() ? 1 : 0) - (drop_right() ? 1 : 0); }
+  // N = p n - 1 (Dirichlet) / p n + 1 (Neumann) / p n (mixed)
   int N() const { return nh() + (p - 1) * n; }
   // global index of the hat at node t (0..n), -1 if dropped; degree-major
   // ordering [H | W_0 | W_1 | ...] of P:L169-L171
   int hat(int node) const {
-    if (bc == 0) return (node == 0 || node == n) ? -1 : node - 1;
-    return node;
+    if ((node == 0 && drop_left()) || (node == n && drop_right())) return -1;
+    return node - (drop_left() ? 1 : 0);
   }
   int bub(int k, int e) const { return nh() + k * n + e; }
   double delta(int e) const { return x[e + 1] - x[e]; }
@@ -72,7 +76,7 @@ struct Space {
 Space make_space(const double* xs, int n, int p, int bc) {
   if (n < 1) throw std::invalid_argument("n < 1");
   if (p < 2) throw std::invalid_argument("p < 2");
-  if (bc != 0 && bc != 1) throw std::invalid_argument("bc");
+  if (bc < 0 || bc > 3) throw std::invalid_argument("bc");
   Space s;
   s.n = n;
   s.p = p;
@@ -407,7 +411,9 @@ void spectrum(const Ops1D& o, double omega, double lam[2]) {
   const Space& s = o.s;
   const double pi = 3.14159265358979323846;
   const double L = s.x[s.n] - s.x[0];
-  lam[0] = (s.bc == 0) ? pi * pi / (L * L) + omega * omega / 2.0 : omega * omega / 2.0;
+  // closed-form lower bounds of the continuous spectrum (reading R4): Dirichlet
+  // pi^2/L^2, Neumann 0, mixed Dirichlet/Neumann pi^2/(4 L^2) (quarter wave)
+  lam[0] = (s.bc == 0 ? pi * pi / (L * L) : s.bc == 1 ? 0.0 : pi * pi / (4.0 * L * L)) + omega * omega / 2.0;
   // initial upper bracket: Lemma 5.2, lambda^{-1} <= (24p^4 + w^2 h^2)/(2h^2)
   double h = s.delta(0);
   for (int e = 1; e < s.n; ++e) h = std::min(h, s.delta(e));
@@ -604,12 +610,25 @@ struct Problem {
   double omega, tol;
 };
 
+/* 2D boundary code: 0..3 = the same 1D code in both directions; 16 + bx + 4 by
+ * = per direction (bx, by in 0..3) */
+void split_bc(int bc, int& bx, int& by) {
+  if (bc >= 16) {
+    bx = (bc - 16) & 3;
+    by = ((bc - 16) >> 2) & 3;
+  } else {
+    bx = by = bc;
+  }
+}
+
 int make_problem(const double* xs, int nx, int px, const double* ys, int ny, int py, double omega, int bc,
                  double tol, Problem& P) {
-  if (bc == 1 && omega == 0.0) throw std::invalid_argument("Neumann requires omega != 0 (P:L812)");
+  int bx, by;
+  split_bc(bc, bx, by);
+  if ((bx == 1 || by == 1) && omega == 0.0) throw std::invalid_argument("Neumann requires omega != 0 (P:L812)");
   if (!(tol > 0.0 && tol < 1.0)) throw std::invalid_argument("tol not in (0,1)");
-  P.ox = make_ops(make_space(xs, nx, px, bc), omega);
-  P.oy = make_ops(make_space(ys, ny, py, bc), omega);
+  P.ox = make_ops(make_space(xs, nx, px, bx), omega);
+  P.oy = make_ops(make_space(ys, ny, py, by), omega);
   P.omega = omega;
   P.tol = tol;
   return 0;
@@ -628,7 +647,10 @@ const char* oracle_last_error(void) { return g_err.c_str(); }
 int oracle_threads(void) { return omp_get_max_threads(); }
 
 /* N of the 1D space */
-int oracle_dim(int n, int p, int bc) { return (bc == 0 ? n - 1 : n + 1) + (p - 1) * n; }
+int oracle_dim(int n, int p, int bc) {
+  const int nh = n + 1 - ((bc == 0 || bc == 2) ? 1 : 0) - ((bc == 0 || bc == 3) ? 1 : 0);
+  return nh + (p - 1) * n;
+}
 
 /* Dense alpha*K + beta*M (N x N, row-major) for tests on small N. */
 int oracle_operator_dense(const double* xs, int n, int p, int bc, double alpha, double beta, double* out) {
@@ -726,7 +748,7 @@ int oracle_solve1d(const double* xs, int n, int p, int bc, double alpha, double 
 int oracle_spectrum(const double* xs, int n, int p, int bc, double omega, double* lam) {
   try {
     Space s = make_space(xs, n, p, bc);
-    if (bc == 1 && omega == 0.0) return fail("Neumann requires omega != 0", -1);
+    if (bc == 1 && omega == 0.0) return fail("Neumann requires omega != 0", -1);  // (mixed ends are definite)
     Ops1D o = make_ops(s, omega);
     spectrum(o, omega, lam);
     return 0;
@@ -853,7 +875,9 @@ int oracle_apply(const double* xs, int nx, int px, const double* ys, int ny, int
 int oracle_load(const double* xs, int nx, int px, const double* ys, int ny, int py, int bc, const double* Fleg,
                 double* G) {
   try {
-    Space sx = make_space(xs, nx, px, bc), sy = make_space(ys, ny, py, bc);
+    int bx, by;
+    split_bc(bc, bx, by);
+    Space sx = make_space(xs, nx, px, bx), sy = make_space(ys, ny, py, by);
     const std::vector<double> R_x = local_R(px), R_y = local_R(py);
     // global sparse Z = M_P R as rows (Legendre index) -> (dof, value)
     auto build = [](const Space& s, const std::vector<double>& Rl) {
@@ -904,7 +928,9 @@ int oracle_load(const double* xs, int nx, int px, const double* ys, int ny, int 
 int oracle_unload(const double* xs, int nx, int px, const double* ys, int ny, int py, int bc, const double* U,
                   double* Cleg) {
   try {
-    Space sx = make_space(xs, nx, px, bc), sy = make_space(ys, ny, py, bc);
+    int bx, by;
+    split_bc(bc, bx, by);
+    Space sx = make_space(xs, nx, px, bx), sy = make_space(ys, ny, py, by);
     const std::vector<double> R_x = local_R(px), R_y = local_R(py);
     // global sparse R as rows (Legendre index) -> (dof, value)
     auto build = [](const Space& s, const std::vector<double>& Rl) {

@@ -14,8 +14,15 @@ import numpy as np
 from scipy.special import eval_jacobi
 
 
+def _ends(bc):
+    """(left end Dirichlet?, right end Dirichlet?) for the 1D codes
+    0 = Dirichlet, 1 = Neumann, 2 = Dirichlet/Neumann, 3 = Neumann/Dirichlet."""
+    return {0: (True, True), 1: (False, False), 2: (True, False), 3: (False, True)}[bc]
+
+
 def nhats(n, bc):
-    return n - 1 if bc == 0 else n + 1
+    dl, dr = _ends(bc)
+    return n + 1 - int(dl) - int(dr)
 
 
 def ndofs(n, p, bc):
@@ -23,9 +30,10 @@ def ndofs(n, p, bc):
 
 
 def hat_index(node, n, bc):
-    if bc == 0:
-        return -1 if node in (0, n) else node - 1
-    return node
+    dl, dr = _ends(bc)
+    if (node == 0 and dl) or (node == n and dr):
+        return -1
+    return node - int(dl)
 
 
 def bubble_ref(k, t):

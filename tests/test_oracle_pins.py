@@ -50,13 +50,13 @@ def test_reference_element_values():
                 assert M[i, j] == 0.0
 
 
-@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
 @pytest.mark.parametrize("mi", range(len(MESHES)))
 def test_operators_vs_quadrature(mi, bc):
     """K = <phi', phi'>, M = <phi, phi> against Gauss
     quadrature with the Jacobi definition of W_k."""
     xs, p = MESHES[mi]
-    if bc == 0 and xs.size == 2 and p < 2:
+    if bc != 1 and xs.size == 2 and p < 2:
         pytest.skip()
     Kq, Mq = fem_ref.assemble_quad(xs, p, bc)
     K = oracle.operator_dense(xs, p, bc, 1.0, 0.0)
@@ -65,7 +65,7 @@ def test_operators_vs_quadrature(mi, bc):
     assert np.abs(K - Kq).max() <= 1e-12 * np.abs(Kq).max()
 
 
-@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
 def test_b3_sparsity(bc):
     """B^3-Arrowhead structure (Def. 4.1): K tridiagonal on hats
     and diagonal on bubbles; in M every block outside the first
@@ -99,10 +99,13 @@ def test_b3_sparsity(bc):
 
 
 def test_dimension_formula():
-    """N = p n - 1 (Dirichlet); p n + 1 for the full basis C."""
+    """N = p n - 1 (Dirichlet); p n + 1 for the full basis C; p n
+    with one Dirichlet and one Neumann end (mixed, NEXT-1)."""
     for n, p in [(1, 2), (4, 8), (16, 32), (3, 5)]:
         assert oracle.dim(n, p, 0) == p * n - 1
         assert oracle.dim(n, p, 1) == p * n + 1
+        assert oracle.dim(n, p, 2) == p * n
+        assert oracle.dim(n, p, 3) == p * n
 
 
 # --------------------------------------------------------- reverse Cholesky
@@ -159,6 +162,8 @@ SPEC_CASES = [
     (rand_mesh(4, 0, 2), 5, 1, 1.0),
     (W.graded_mesh(0, 1, 8, 0.5), 6, 1, 1.0),
     (np.linspace(0, 1, 3), 3, 1, 3.0),
+    (rand_mesh(5, 0, 2), 6, 2, 0.0),  # mixed Dirichlet / Neumann
+    (W.graded_mesh(0, 1, 6, 0.5), 5, 3, 2.0),
 ]
 
 
@@ -185,10 +190,16 @@ def test_spectrum_vs_eigh(case):
         c[: n + 1] = 1.0
         assert np.abs(K @ c).max() <= 1e-13 * np.abs(K).max()
         assert lam[0] == pytest.approx(om * om / 2, rel=1e-15)
-    else:
+    elif bc == 0:
         # Poincare: discrete lambda_min >= pi^2/L^2 + w^2/2
         L = xs[-1] - xs[0]
         assert lam[0] == pytest.approx(math.pi ** 2 / L ** 2 + om * om / 2, rel=1e-15)
+    else:
+        # mixed ends: the continuous first eigenvalue is the quarter wave
+        # pi^2/(4 L^2) + w^2/2, a lower bound of the conforming discrete one
+        L = xs[-1] - xs[0]
+        assert lam[0] == pytest.approx(math.pi ** 2 / (4 * L ** 2) + om * om / 2, rel=1e-15)
+        assert ev[0] <= lam[0] * (1 + 1e-2)  # and close to it at this resolution
 
 
 @pytest.mark.parametrize("case", range(len(SPEC_CASES)))
@@ -201,8 +212,10 @@ def test_lemma52_containment(case):
     lo = 2 * h * h / (24 * p ** 4 + om * om * h * h)
     if bc == 0:
         C = min(L * L / math.pi ** 2, max(1.0, 2.0 / om ** 2) if om else math.inf)
-    else:
+    elif bc == 1:
         C = max(1.0, 2.0 / om ** 2)
+    else:  # mixed ends: the quarter-wave Poincare constant (4 L^2 / pi^2)
+        C = min(4 * L * L / math.pi ** 2, max(1.0, 2.0 / om ** 2) if om else math.inf)
     assert 1.0 / lam[1] >= lo * (1 - 1e-12)
     assert 1.0 / lam[0] <= C * (1 + 1e-12)
 
@@ -301,12 +314,14 @@ ADI_CASES = [
     (rand_mesh(3), 5, rand_mesh(2, 0, 3), 6, 1.0, 1),
     (W.graded_mesh(0, 1, 6, 0.5), 5, W.graded_mesh(0, 1, 6, 0.5), 5, 1.0, 1),
     (np.linspace(-1, 1, 3), 7, np.linspace(-1, 1, 3), 7, 10.0, 0),
+    (rand_mesh(3), 6, rand_mesh(4, 0, 2), 5, 0.0, oracle.bc2d(2, 3)),  # mixed ends, per direction (NEXT-1)
 ]
 
 
 def _dense_sylvester(xs, px, ys, py, om, bc, G):
-    Kx, Mx = oracle.operator_dense(xs, px, bc, 1, 0), oracle.operator_dense(xs, px, bc, 0, 1)
-    Ky, My = oracle.operator_dense(ys, py, bc, 1, 0), oracle.operator_dense(ys, py, bc, 0, 1)
+    bx, by = oracle.split_bc(bc)
+    Kx, Mx = oracle.operator_dense(xs, px, bx, 1, 0), oracle.operator_dense(xs, px, bx, 0, 1)
+    Ky, My = oracle.operator_dense(ys, py, by, 1, 0), oracle.operator_dense(ys, py, by, 0, 1)
     Ax, Ay = Kx + om * om / 2 * Mx, Ky + om * om / 2 * My
     Big = np.kron(Ax, My) + np.kron(Mx, Ay)  # vec_row(A_x U M_y + M_x U A_y)
     U = np.linalg.solve(Big, G.reshape(-1)).reshape(G.shape)
@@ -320,7 +335,7 @@ def test_adi_lemma51(case, tol):
     M_x = V^T V, M_y = L^T L, U the dense Kronecker solution of
     eq. adi:poisson (P:L658-L664)."""
     xs, px, ys, py, om, bc = ADI_CASES[case]
-    Nx, Ny = oracle.dim(xs.size - 1, px, bc), oracle.dim(ys.size - 1, py, bc)
+    Nx, Ny = oracle.dim(xs.size - 1, px, oracle.split_bc(bc)[0]), oracle.dim(ys.size - 1, py, oracle.split_bc(bc)[1])
     G = RNG.standard_normal((Nx, Ny))
     Us, Mx, My, _, _ = _dense_sylvester(xs, px, ys, py, om, bc, G)
     U, J = oracle.adi_solve(xs, px, ys, py, om, bc, tol, G)
@@ -337,7 +352,7 @@ def test_adi_contraction_per_J():
     for J'), err <= 4 exp(-pi^2 J'/log(16 gamma)) (FT20 Th. 2.1 as used at
     P:L751-L753)."""
     xs, px, ys, py, om, bc = ADI_CASES[0]
-    Nx, Ny = oracle.dim(xs.size - 1, px, bc), oracle.dim(ys.size - 1, py, bc)
+    Nx, Ny = oracle.dim(xs.size - 1, px, oracle.split_bc(bc)[0]), oracle.dim(ys.size - 1, py, oracle.split_bc(bc)[1])
     G = RNG.standard_normal((Nx, Ny))
     Us, Mx, My, _, _ = _dense_sylvester(xs, px, ys, py, om, bc, G)
     V, L = np.linalg.cholesky(Mx).T, np.linalg.cholesky(My).T
@@ -366,7 +381,7 @@ def test_adi_one_point_spectrum(swap):
     b = (rand_mesh(3, 0, 2), 4)     # N = 11
     (xs, px), (ys, py) = (b, a) if swap else (a, b)
     om, bc = 0.7, 0
-    Nx, Ny = oracle.dim(xs.size - 1, px, bc), oracle.dim(ys.size - 1, py, bc)
+    Nx, Ny = oracle.dim(xs.size - 1, px, oracle.split_bc(bc)[0]), oracle.dim(ys.size - 1, py, oracle.split_bc(bc)[1])
     G = RNG.standard_normal((Nx, Ny))
     Us, _, _, _, _ = _dense_sylvester(xs, px, ys, py, om, bc, G)
     pl = oracle.plan(xs, px, ys, py, om, bc, 1e-10)
@@ -391,7 +406,7 @@ def test_adi_1x1():
 def test_adi_zero_and_linear():
     """F = 0 => U = 0; the solve is linear in F."""
     xs, px, ys, py, om, bc = ADI_CASES[2]
-    Nx, Ny = oracle.dim(xs.size - 1, px, bc), oracle.dim(ys.size - 1, py, bc)
+    Nx, Ny = oracle.dim(xs.size - 1, px, oracle.split_bc(bc)[0]), oracle.dim(ys.size - 1, py, oracle.split_bc(bc)[1])
     U0, _ = oracle.adi_solve(xs, px, ys, py, om, bc, 1e-10, np.zeros((Nx, Ny)))
     assert np.all(U0 == 0)
     G1, G2 = RNG.standard_normal((2, Nx, Ny))
@@ -407,8 +422,9 @@ def test_apply_vs_dense(case):
     """A_x U M_y + M_x U A_y equals the dense Kronecker matvec built from
     the quadrature operators."""
     xs, px, ys, py, om, bc = ADI_CASES[case]
-    Kx, Mx = fem_ref.assemble_quad(xs, px, bc)
-    Ky, My = fem_ref.assemble_quad(ys, py, bc)
+    bx, by = oracle.split_bc(bc)
+    Kx, Mx = fem_ref.assemble_quad(xs, px, bx)
+    Ky, My = fem_ref.assemble_quad(ys, py, by)
     Ax, Ay = Kx + om * om / 2 * Mx, Ky + om * om / 2 * My
     U = RNG.standard_normal((Kx.shape[0], Ky.shape[0]))
     F = oracle.apply(xs, px, ys, py, om, bc, U)
@@ -432,7 +448,7 @@ def test_load_constant_one():
     np.testing.assert_allclose(G, np.outer(g1, g1), atol=1e-15)
 
 
-@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
 def test_load_vs_quadrature(bc):
     """G_ij = <phi_i psi_j, f> for a random
     piecewise-polynomial f, by tensor quadrature."""
@@ -452,7 +468,7 @@ def test_load_vs_quadrature(bc):
     assert np.abs(G - Gq).max() <= 1e-13 * np.abs(Gq).max()
 
 
-@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
 def test_unload_pointwise(bc):
     """C_leg = R_x U R_y^T reproduces the FEM function pointwise: the
     Legendre series with coefficients C_leg equals sum U_ij phi_i(x) psi_j(y)
@@ -474,7 +490,7 @@ def test_unload_pointwise(bc):
     assert np.abs(u_fem - u_leg).max() <= 1e-13 * np.abs(u_fem).max()
 
 
-@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
 def test_load_of_unload_is_mass(bc):
     """load(unload(U)) = R^T M_P R U R^T M_P R = M_x U M_y (Gram matrix of the
     basis), M from the quadrature reference."""
