@@ -47,12 +47,24 @@ extern "C" {
 
 typedef struct hpfem_plan_s* hpfem_plan_t; /* opaque; owned by the library */
 
-enum { HPFEM_BC_DIRICHLET = 0, HPFEM_BC_NEUMANN = 1 }; /* same BC on all four sides */
+/* Boundary conditions (zero data, eq. poisson).  A 1D
+ * code fixes both ends of one direction: a Dirichlet end drops its boundary
+ * hat (basis Q), a Neumann end keeps it (basis C), so N =
+ * p n - 1, p n + 1 or p n (mixed).  A 2D `bc` argument is either a 1D code
+ * (the same in both directions) or HPFEM_BC_2D(bc_x, bc_y), per direction. */
+enum {
+  HPFEM_BC_DIRICHLET = 0,          /* both ends Dirichlet */
+  HPFEM_BC_NEUMANN = 1,            /* both ends Neumann (needs w != 0) */
+  HPFEM_BC_DIRICHLET_NEUMANN = 2,  /* Dirichlet at a (resp. c), Neumann at b (resp. d) */
+  HPFEM_BC_NEUMANN_DIRICHLET = 3   /* Neumann at a (resp. c), Dirichlet at b (resp. d) */
+};
+#define HPFEM_BC_2D(bc_x, bc_y) (16 + (bc_x) + 4 * (bc_y))
 
 enum {
   HPFEM_OK = 0,
   HPFEM_EINVAL = -1,   /* bad argument: n < 1, p < 2, non-increasing breakpoints,
-                          tol not in (0,1), Neumann with w = 0, aliasing */
+                          tol not in (0,1), Neumann with w = 0, aliasing,
+                          bc not a 1D code or HPFEM_BC_2D(0..3, 0..3) */
   HPFEM_ENOTPD = -2,   /* a non-positive pivot in a reverse Cholesky factorisation */
   HPFEM_ECUDA = -3,    /* CUDA runtime / launch error, or no sm_100 device */
   HPFEM_ENOMEM = -4,   /* device allocation failed */
@@ -63,7 +75,7 @@ enum {
  * hpfem_plan -- Alg. 2 "Precomputation" on a uniform mesh.
  *   n_x elements on [a,b] of degree p_x; n_y elements on [c,d] of degree p_y
  *   (p >= 2: hats plus bubbles W_0..W_{p-2}); omega = w of eq. poisson;
- *   bc = HPFEM_BC_*; tol = epsilon of Lemma 5.1, 0 < tol < 1.
+ *   bc = HPFEM_BC_* or HPFEM_BC_2D(bc_x, bc_y); tol = epsilon of Lemma 5.1, 0 < tol < 1.
  * Builds the 1D operators (closed forms of App. A), the
  * spectral intervals [lambda_min, lambda_max] of (A_d, M_d) (DESIGN.md
  * reading R4), gamma, J = ceil(log(16 gamma) log(4/tol)/pi^2), the
@@ -142,11 +154,12 @@ int hpfem_unload(hpfem_plan_t plan, const double* U, double* C_leg, void* cuda_s
 /*
  * 1D solver workload (NEXT-2 of SURVEY 8(f); the paper's Fig. 1):
  * batched solves of the 1D screened Poisson discretisation
- *        (K + w^2 M) u = f      (Dirichlet basis Q or Neumann C)
+ *        (K + w^2 M) u = f      (Dirichlet basis Q, Neumann C or mixed)
  * with the reverse Cholesky factor of Algorithm 1 in static-
  * condensation form (one CTA per right-hand side).
  *   hpfem_plan1d: breakpoints xs[0..n] (host, strictly increasing), degree
- *     p >= 2, bc, omega (Neumann needs omega != 0); factors on the device and
+ *     p >= 2, bc = a 1D code HPFEM_BC_DIRICHLET .. HPFEM_BC_NEUMANN_DIRICHLET,
+ *     omega (Neumann at both ends needs omega != 0); factors on the device and
  *     synchronises cuda_stream once.  ENOTPD on a non-positive pivot.
  *   hpfem_solve1d: F, U device, nrhs x N row-major (N from hpfem_plan1d_info,
  *     dofs ordered as the 2D arrays' rows: hats, then degree-major bubbles);

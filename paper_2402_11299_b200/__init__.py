@@ -20,6 +20,15 @@ LIB_PATH = os.path.join(_HERE, "libhpfem_b200.so")
 
 HPFEM_BC_DIRICHLET = 0
 HPFEM_BC_NEUMANN = 1
+HPFEM_BC_DIRICHLET_NEUMANN = 2
+HPFEM_BC_NEUMANN_DIRICHLET = 3
+
+
+def HPFEM_BC_2D(bc_x: int, bc_y: int) -> int:
+    """Per-direction 2D boundary code (include/hpfem.h HPFEM_BC_2D)."""
+    return 16 + bc_x + 4 * bc_y
+
+
 HPFEM_OK, HPFEM_EINVAL, HPFEM_ENOTPD, HPFEM_ECUDA, HPFEM_ENOMEM, HPFEM_ENUMERIC = 0, -1, -2, -3, -4, -5
 _NAMES = {-1: "EINVAL", -2: "ENOTPD", -3: "ECUDA", -4: "ENOMEM", -5: "ENUMERIC"}
 

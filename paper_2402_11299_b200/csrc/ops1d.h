@@ -54,13 +54,19 @@ HD double s_hat_diag_elem(double kap, double sig, double delta) { return kap / d
 HD double s_hat_off_elem(double kap, double sig, double delta) { return -kap / delta + sig * (delta / 6.0); }
 
 /* index helpers (degree-major / element-minor ordering) */
-HD int n_hats(int n, int bc) { return bc == 0 ? n - 1 : n + 1; }
-/* hat index of mesh node `node` (0..n), -1 if dropped (Dirichlet boundary) */
+/* 1D boundary codes: 0 Dirichlet both ends, 1 Neumann both ends, 2 Dirichlet
+ * left / Neumann right, 3 Neumann left / Dirichlet right.  A Dirichlet end
+ * drops its boundary hat, a Neumann end keeps it (basis C):
+ * the per-side keep/drop mask of P:L430-L435. */
+HD int drop_left(int bc) { return (bc == 0 || bc == 2) ? 1 : 0; }
+HD int drop_right(int bc) { return (bc == 0 || bc == 3) ? 1 : 0; }
+HD int n_hats(int n, int bc) { return n + 1 - drop_left(bc) - drop_right(bc); }
+/* hat index of mesh node `node` (0..n), -1 if dropped (Dirichlet end) */
 HD int hat_of_node(int node, int n, int bc) {
-  if (bc == 0) return (node == 0 || node == n) ? -1 : node - 1;
-  return node;
+  if ((node == 0 && drop_left(bc)) || (node == n && drop_right(bc))) return -1;
+  return node - drop_left(bc);
 }
-HD int node_of_hat(int t, int bc) { return bc == 0 ? t + 1 : t; }
+HD int node_of_hat(int t, int bc) { return t + drop_left(bc); }
 /* chain lengths: parity 0 -> degrees 0,2,4..; parity 1 -> 1,3,5.. (k <= p-2) */
 HD int chain_len(int p, int parity) { return parity == 0 ? p / 2 : (p - 1) / 2; }
 

@@ -41,6 +41,18 @@ int cuda_err(cudaError_t e, const char* where) {
   return set_err(HPFEM_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+/* 2D boundary code -> per-direction 1D codes (include/hpfem.h HPFEM_BC_2D) */
+bool split_bc(int bc, int& bx, int& by) {
+  if (bc >= HPFEM_BC_DIRICHLET && bc <= HPFEM_BC_NEUMANN_DIRICHLET) {
+    bx = by = bc;
+    return true;
+  }
+  if (bc < 16 || bc > 31) return false;
+  bx = (bc - 16) & 3;
+  by = ((bc - 16) >> 2) & 3;
+  return true;
+}
+
 /* host view of one direction */
 struct DirHost {
   int n = 0, p = 0, bc = 0, nh = 0, N = 0, nb = 0;
@@ -133,7 +145,12 @@ void spectral_interval(const DirHost& d, double omega, double lam[2]) {
   }
   const double len = d.xs[d.n] - d.xs[0];
   const double pi = 3.141592653589793238462643383279502884;
-  lam[0] = d.bc == 0 ? pi * pi / (len * len) + hw2 : hw2;
+  // closed-form lower bounds of the continuous spectrum: Dirichlet pi^2/L^2,
+  // Neumann 0 (constants), mixed Dirichlet/Neumann pi^2/(4 L^2) (quarter wave)
+  lam[0] = (d.bc == HPFEM_BC_DIRICHLET ? pi * pi / (len * len)
+            : d.bc == HPFEM_BC_NEUMANN ? 0.0
+                                       : pi * pi / (4.0 * len * len)) +
+           hw2;
   double h = d.delta[0];
   for (double x : d.delta) h = std::min(h, x);
   const double p2 = (double)d.p * d.p;
@@ -395,18 +412,19 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   int rc;
   if ((rc = validate_mesh(xs, nx, px)) != HPFEM_OK) return rc;
   if ((rc = validate_mesh(ys, ny, py)) != HPFEM_OK) return rc;
-  if (bc != HPFEM_BC_DIRICHLET && bc != HPFEM_BC_NEUMANN) return set_err(HPFEM_EINVAL, "bad bc");
+  int bx, by;
+  if (!split_bc(bc, bx, by)) return set_err(HPFEM_EINVAL, "bad bc");
   if (!(tol > 0.0 && tol < 1.0)) return set_err(HPFEM_EINVAL, "tol must lie in (0,1)");
   if (!std::isfinite(omega)) return set_err(HPFEM_EINVAL, "omega not finite");
-  if (bc == HPFEM_BC_NEUMANN && omega == 0.0)
+  if ((bx == HPFEM_BC_NEUMANN || by == HPFEM_BC_NEUMANN) && omega == 0.0)
     return set_err(HPFEM_EINVAL, "Neumann requires omega != 0 (P:L812)");
   int ndev = 0;
   cudaError_t ce = cudaGetDeviceCount(&ndev);
   if (ce != cudaSuccess || ndev == 0) return set_err(HPFEM_ECUDA, "no CUDA device (no CPU fallback)");
 
   hpfem_plan_t pl = new hpfem_plan_s();
-  pl->hx = make_dir(xs, nx, px, bc);
-  pl->hy = make_dir(ys, ny, py, bc);
+  pl->hx = make_dir(xs, nx, px, bx);
+  pl->hy = make_dir(ys, ny, py, by);
   pl->omega = omega;
   pl->tol = tol;
   spectral_interval(pl->hx, omega, pl->lam_x);
@@ -874,7 +892,7 @@ int hpfem_plan1d(const double* xs, int n, int p, int bc, double omega, void* cud
   *out = nullptr;
   int rc;
   if ((rc = validate_mesh(xs, n, p)) != HPFEM_OK) return rc;
-  if (bc != HPFEM_BC_DIRICHLET && bc != HPFEM_BC_NEUMANN) return set_err(HPFEM_EINVAL, "bad bc");
+  if (bc < HPFEM_BC_DIRICHLET || bc > HPFEM_BC_NEUMANN_DIRICHLET) return set_err(HPFEM_EINVAL, "bad bc");
   if (!std::isfinite(omega)) return set_err(HPFEM_EINVAL, "omega not finite");
   if (bc == HPFEM_BC_NEUMANN && omega == 0.0) return set_err(HPFEM_EINVAL, "Neumann requires omega != 0");
   int ndev = 0;

@@ -187,7 +187,7 @@ __device__ __forceinline__ void x_issue(const TmaStepArgs& A, uint32_t gs, unsig
   const int pi = (int)A.fT.div(rest), e_x = rest - pi * x.n;
   const int EG = A.EG;
   const int c0 = P.lay.hb + g * EG * P.lay.Q;
-  const int hc = (y.bc == 0 ? g * EG - 1 : g * EG) & ~1;  // innermost TMA coordinate: 16-byte aligned
+  const int hc = (g * EG - drop_left(y.bc)) & ~1;  // innermost TMA coordinate: 16-byte aligned
   const int row = KR * s < chain_len(x.p, pi) ? KR * s : 0;  // a stage past this parity's chain: any rows (unused)
   unsigned char* st = ring + (size_t)slot * A.stage_bytes;
   if (s == A.S - 1) {  // the tile's chain factors ride with its first stage
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
     const int m = chain_len(x.p, pi);
     const double* fb = fbuf + (ctt & 1) * A.fac_doubles;  // [4c] il, [4c+1] g il, [4c+2] g_prev il
     const bool valid = eo < EG && ky < q && ey < y.n;
-    const int h0 = (y.bc == 0 ? e0 - 1 : e0) & ~1;
+    const int h0 = (e0 - drop_left(y.bc)) & ~1;
     Sten5 st;
     int o0 = 0, o1 = 0, o2 = 0, o3 = 0, o4 = 0;
     const bool wtab = P.wtab != nullptr && MODE == ST_APPLY;
@@ -358,7 +358,7 @@ __device__ __forceinline__ void y_issue(const TmaStepArgs& A, uint32_t gs, unsig
   const int slot = (int)(gs - A.fN.div(gs) * A.nstages);
   const YTile t = y_decode(A, tile);
   const int e0 = t.g * A.EG, kh0 = t.kw * A.R;
-  const int hL = x.bc == 0 ? t.e_x - 1 : t.e_x;
+  const int hL = t.e_x - drop_left(x.bc);
   unsigned char* st = ring + (size_t)slot * A.stage_bytes;
   if (s == A.S - 1) {  // chain factors of the tile's EG elements x 2 parities (one contiguous block)
     const uint32_t fb = tl & 1;

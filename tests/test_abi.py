@@ -78,3 +78,33 @@ def test_refuses_without_device():
     assert rc == -3  # HPFEM_ECUDA
     rc = L.hpfem_plan_mesh(p, 2, 1, p, 2, 4, 0.0, 0, 1e-10, None, ctypes.byref(h))
     assert rc == -1  # HPFEM_EINVAL is checked before touching the device
+
+
+def test_boundary_codes_validated_before_device():
+    """Boundary codes (include/hpfem.h): 0..3 and HPFEM_BC_2D(0..3, 0..3) are
+    accepted (-> ECUDA here, no device); anything else, or a Neumann-only
+    direction with w = 0, is EINVAL before the device is touched."""
+    import paper_2402_11299_b200 as hp
+
+    L = ctypes.CDLL(_lib_path())
+    L.hpfem_plan_mesh.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_int,
+                                  ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                  ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+    xs = np.linspace(0, 1, 3)
+    h = ctypes.c_void_p()
+    p = xs.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    ok = -3 if not __import__("torch").cuda.is_available() else 0
+
+    def rc(bc, om):
+        r = L.hpfem_plan_mesh(p, 2, 4, p, 2, 4, om, bc, 1e-10, None, ctypes.byref(h))
+        if r == 0:
+            ctypes.CDLL(_lib_path()).hpfem_plan_destroy(h)
+        return r
+
+    for bc in (0, 2, 3, hp.HPFEM_BC_2D(2, 3), hp.HPFEM_BC_2D(0, 2)):
+        assert rc(bc, 0.0) == ok, bc
+    for bc in (1, hp.HPFEM_BC_2D(1, 1), hp.HPFEM_BC_2D(3, 1)):
+        assert rc(bc, 1.0) == ok, bc
+        assert rc(bc, 0.0) == -1, bc  # a Neumann-only direction needs w != 0
+    for bc in (-1, 4, 15, 32, hp.HPFEM_BC_2D(0, 4)):
+        assert rc(bc, 1.0) == -1, bc

@@ -41,7 +41,14 @@ SMALL = [
     (np.linspace(0, 1, 3), 150, np.linspace(0, 1, 2), 140, 0.5, 0, 1e-8),  # chains > 64 (long path)
     (rmesh(1, 0, 1, 5), 2, rmesh(3, 0, 2, 6), 24, 0.7, 0, 1e-10),  # N_x = 1 only: reading R15
     (rmesh(4, 0, 1, 7), 24, rmesh(1, 0, 2, 8), 2, 0.7, 0, 1e-10),  # N_y = 1 only
+    # mixed Dirichlet / Neumann ends (hat keep/drop mask, NEXT-1)
+    (rmesh(4, 0, 1, 11), 7, rmesh(5, 0, 2, 12), 6, 0.0, oracle.bc2d(2, 3), 1e-12),  # 12
+    (W.graded_mesh(0, 1, 6, 0.6), 8, np.linspace(0, 1, 5), 9, 1.0, oracle.bc2d(1, 0), 1e-10),
+    (np.linspace(0, 1, 3), 5, np.array([0.0, 1.0]), 4, 0.0, 2, 1e-12),  # n_y = 1 mixed: one hat
+    (rmesh(6, 0, 1, 13), 20, rmesh(5, 0, 1, 14), 18, 0.5, oracle.bc2d(3, 2), 1e-10),  # TMA shapes
+    (rmesh(3, 0, 1, 15), 34, rmesh(7, 0, 3, 16), 20, 2.0, oracle.bc2d(2, 1), 1e-10),
 ]
+MIXED = list(range(12, len(SMALL)))
 
 
 @pytest.fixture(params=["tma", "ldg"])
@@ -72,14 +79,15 @@ def test_small_cases(case, kernel_path):
     assert l2 <= L2_TOL
 
 
-@pytest.mark.parametrize("case", [3, 4, 5, 7])
+@pytest.mark.parametrize("case", [3, 4, 5, 7, 12, 13, 14])
 def test_lemma51_against_dense(case):
     """The GPU solution itself meets Lemma 5.1 against the dense
     Kronecker solution of eq. adi:poisson."""
     xs, px, ys, py, om, bc, tol = SMALL[case]
+    bx, by = oracle.split_bc(bc)
     plan = gpu_plan(xs, px, ys, py, om, bc, tol)
-    Kx, Mx = oracle.operator_dense(xs, px, bc, 1, 0), oracle.operator_dense(xs, px, bc, 0, 1)
-    Ky, My = oracle.operator_dense(ys, py, bc, 1, 0), oracle.operator_dense(ys, py, bc, 0, 1)
+    Kx, Mx = oracle.operator_dense(xs, px, bx, 1, 0), oracle.operator_dense(xs, px, bx, 0, 1)
+    Ky, My = oracle.operator_dense(ys, py, by, 1, 0), oracle.operator_dense(ys, py, by, 0, 1)
     Ax, Ay = Kx + om * om / 2 * Mx, Ky + om * om / 2 * My
     G = RNG.standard_normal((plan.Nx, plan.Ny))
     Us = np.linalg.solve(np.kron(Ax, My) + np.kron(Mx, Ay), G.reshape(-1)).reshape(G.shape)
@@ -142,8 +150,10 @@ def test_config_unload(i):
 
 
 def test_unload_small_shapes():
-    """Edge shapes: p = 2 (no odd bubbles), one element, Neumann / Dirichlet."""
-    for (n, p, bc) in [(1, 2, 0), (1, 2, 1), (3, 3, 0), (2, 9, 1), (5, 4, 0)]:
+    """Edge shapes: p = 2 (no odd bubbles), one element, Neumann / Dirichlet /
+    mixed ends."""
+    for (n, p, bc) in [(1, 2, 0), (1, 2, 1), (3, 3, 0), (2, 9, 1), (5, 4, 0), (1, 3, 2), (4, 5, 3),
+                       (3, 6, oracle.bc2d(2, 1))]:
         xs = rmesh(n, seed=n + p)
         ys = rmesh(n + 1, 0.0, 2.0, seed=p)
         om = 1.0 if bc else 0.0
@@ -164,6 +174,66 @@ def test_config_apply(i):
     F = gpu_apply(plan, U)
     Fref = oracle.apply(xs, c.px, ys, c.py, c.omega, c.bc, U)
     assert np.abs(F - Fref).max() <= 1e-12 * np.abs(Fref).max()
+
+
+@pytest.mark.parametrize("case", MIXED)
+def test_mixed_apply_load(case):
+    """hpfem_apply and hpfem_load with mixed Dirichlet / Neumann ends vs the
+    oracle (the hat keep/drop mask of P:L430-L435)."""
+    xs, px, ys, py, om, bc, tol = SMALL[case]
+    plan = gpu_plan(xs, px, ys, py, om, bc, tol)
+    U = W.random_field((plan.Nx, plan.Ny), 40 + case)
+    F = gpu_apply(plan, U)
+    Fref = oracle.apply(xs, px, ys, py, om, bc, U)
+    assert np.abs(F - Fref).max() <= 1e-12 * np.abs(Fref).max()
+    Fleg = W.random_field(((px + 1) * (xs.size - 1), (py + 1) * (ys.size - 1)), 50 + case)
+    G = gpu_load(plan, Fleg)
+    Gref = oracle.load(xs, px, ys, py, bc, Fleg)
+    assert np.abs(G - Gref).max() <= 1e-14 * np.abs(Gref).max()
+
+
+def test_mixed_manufactured_solution():
+    """The quarter-wave mode u = sin(pi x / 2) sin(pi y / 2) on [0,1]^2 is zero
+    at x = 0 and y = 0 (Dirichlet) and has zero normal derivative at x = 1 and
+    y = 1 (Neumann): -Delta u + w^2 u = (pi^2/2 + w^2) u.  The GPU
+    solve of the loaded right-hand side converges exponentially in p to the
+    exact solution in L2 (checked through the piecewise-Legendre coefficients
+    of hpfem_unload against Gauss quadrature of u)."""
+    torch = torch_cuda()
+    import paper_2402_11299_b200 as hp
+
+    om = 1.0
+    lam = np.pi ** 2 / 2 + om ** 2
+    n = 3
+    xs = np.linspace(0.0, 1.0, n + 1)
+    errs = []
+    for p in (4, 8, 12):
+        # Legendre coefficients of f = lam * u per element (Gauss-Legendre projection)
+        tq, wq = np.polynomial.legendre.leggauss(p + 20)
+        Pm = np.stack([np.polynomial.legendre.Legendre.basis(k)(tq) for k in range(p + 1)])  # (p+1, nq)
+        cf = np.zeros(((p + 1) * n,))
+        cu = np.zeros(((p + 1) * n,))
+        for e in range(n):
+            x = xs[e] + (tq + 1) * (xs[e + 1] - xs[e]) / 2
+            for k in range(p + 1):
+                cu[k * n + e] = (2 * k + 1) / 2 * np.sum(wq * Pm[k] * np.sin(np.pi * x / 2))
+        Cu = np.outer(cu, cu)  # separable u: coefficients of the L2 projection
+        Fleg = lam * Cu
+        plan = hp.Plan(xs, p, xs, p, om, hp.HPFEM_BC_DIRICHLET_NEUMANN, 1e-12)
+        Fd = torch.from_numpy(Fleg).cuda()
+        G = torch.empty((plan.Nx, plan.Ny), dtype=torch.float64, device="cuda")
+        U = torch.empty_like(G)
+        plan.load(Fd, G)
+        plan.solve(G, U)
+        C = torch.empty_like(Fd)
+        plan.unload(U, C)
+        torch.cuda.synchronize()
+        D = C.cpu().numpy() - Cu  # Legendre coefficients of u_h - Pi u (Pi: L2 projection)
+        wts = np.array([(xs[e + 1] - xs[e]) / (2 * k + 1) for k in range(p + 1) for e in range(n)])
+        errs.append(float(np.sqrt(np.einsum("i,j,ij->", wts, wts, D * D))))
+        plan.close()
+    print("mixed manufactured L2 errors", errs)
+    assert errs[1] < 1e-3 * errs[0] and errs[2] < 1e-9
 
 
 @pytest.mark.parametrize("i", [1, 2, 3, 4])
@@ -284,6 +354,9 @@ CASES_1D = [
     (rmesh(17, 0, 1, 21), 33, 1, 0.5),            # odd p, Neumann
     (W.graded_mesh(0, 1, 24, 0.7), 16, 0, 3.0),   # graded
     (np.linspace(0, 1, 301), 3, 0, 1.0),          # many elements: long hat system
+    (rmesh(9, 0, 1, 31), 10, 2, 0.0),             # mixed: Dirichlet left, Neumann right
+    (np.array([0.0, 1.0]), 5, 3, 0.0),            # mixed, one element: one hat
+    (rmesh(40, 0, 2, 32), 3, 3, 2.0),             # mixed, Neumann left
 ]
 
 
