@@ -6,6 +6,10 @@ cpu_baseline / --impl reference legs of bench.py.  The product package
 product.  Every function cites the passage of PAPER.md it follows in the C++
 source; readings are listed in DESIGN.md.
 
+NEXT-3 (transforms, variable coefficient, PCG) lives in oracle/transforms.py
+(numpy), pinned by tests/test_oracle_transforms.py (incl. the paper's
+Table 1 iteration counts).
+
 Parity status: every function exported here is pinned by tests/test_oracle_pins.py
 against values fixed by the paper or by mathematics (quadrature, dense LAPACK,
 mpmath, closed forms); none is "parity unpinned".
