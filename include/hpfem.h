@@ -152,6 +152,51 @@ int hpfem_load(hpfem_plan_t plan, const double* F_leg, double* G, void* cuda_str
 int hpfem_unload(hpfem_plan_t plan, const double* U, double* C_leg, void* cuda_stream);
 
 /*
+ * Transforms and the variable-coefficient solver (NEXT-3 of SURVEY 8(f);
+ * Section 6 P:L897-L948 and Section 7).
+ *
+ * Grid: on every element the p + 1 Chebyshev points of the first kind
+ * sin(pi (m - 2k + 1)/(2m)), k = 1..m, m = p + 1 (P:L908-L910 with m = p + 1
+ * points for degree p: DESIGN.md R17), affinely mapped.  Grid arrays are
+ * ((p_x+1) n_x) x ((p_y+1) n_y) like F_leg / C_leg: row i n_x + e = point i
+ * (descending in x) of x-element e (R18).
+ *
+ * hpfem_grid       -- host arrays x[(p_x+1) n_x], y[(p_y+1) n_y] of the grid
+ *                     coordinates (computed on the host, no device work).
+ * hpfem_transform  -- C = F_x V F_y^T: values on the grid ->
+ *                     Legendre coefficients of the piecewise tensor
+ *                     interpolant.  V, C device, grid / F_leg layout.
+ * hpfem_itransform -- V = F_x^{-1} C F_y^{-T}: Legendre
+ *                     coefficients -> values on the grid.
+ * hpfem_varcoef_apply -- F = A_x U M_y + M_x U A_y + <v, c u>, the last term
+ *                     by eq. (evaluation) (R19):
+ *                     R_x^T M_P F_x [c o (F_x^{-1} R_x U R_y^T F_y^{-T})]
+ *                     F_y^T M_P R_y, with c given on the grid (device,
+ *                     grid layout).  U, F: device N_x x N_y; F must not
+ *                     overlap U or cgrid.
+ * hpfem_pcg        -- solves varcoef_apply(U) = G by conjugate gradients
+ *                     preconditioned with this plan's ADI solve (the plan's
+ *                     tol is the preconditioner tolerance, 1e-4 in the paper,
+ *                     P:L1008); U_0 = 0, stops when ||r||_2 <= rtol ||G||_2
+ *                     (R20) or after maxit iterations.  *iters = iterations
+ *                     (operator applications), *relres = final ||r||/||G||
+ *                     (either pointer may be null).  Synchronises cuda_stream
+ *                     once per iteration (the residual test); uses the plan's
+ *                     solve workspace, so it must not run concurrently with
+ *                     hpfem_solve on the same plan.  ENUMERIC on a non-finite
+ *                     residual (e.g. an indefinite operator).
+ * The transform matrices and scratch (2 grid arrays; 4 N_x N_y vectors for
+ * PCG) are allocated on first use and owned by the plan.  EINVAL on null or
+ * overlapping buffers, ENOMEM / ECUDA as above.
+ */
+int hpfem_grid(hpfem_plan_t plan, double* x, double* y);
+int hpfem_transform(hpfem_plan_t plan, const double* V, double* C, void* cuda_stream);
+int hpfem_itransform(hpfem_plan_t plan, const double* C, double* V, void* cuda_stream);
+int hpfem_varcoef_apply(hpfem_plan_t plan, const double* cgrid, const double* U, double* F, void* cuda_stream);
+int hpfem_pcg(hpfem_plan_t plan, const double* cgrid, const double* G, double* U, double rtol, int maxit, int* iters,
+              double* relres, void* cuda_stream);
+
+/*
  * 1D solver workload (NEXT-2 of SURVEY 8(f); the paper's Fig. 1):
  * batched solves of the 1D screened Poisson discretisation
  *        (K + w^2 M) u = f      (Dirichlet basis Q, Neumann C or mixed)

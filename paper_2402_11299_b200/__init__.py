@@ -59,6 +59,11 @@ def _load():
     L.hpfem_load.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_unload.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_solve_batched.argtypes = [_vp, _i, _vp, _vp, _vp]
+    L.hpfem_grid.argtypes = [_vp, _dp, _dp]
+    L.hpfem_transform.argtypes = [_vp, _vp, _vp, _vp]
+    L.hpfem_itransform.argtypes = [_vp, _vp, _vp, _vp]
+    L.hpfem_varcoef_apply.argtypes = [_vp, _vp, _vp, _vp, _vp]
+    L.hpfem_pcg.argtypes = [_vp, _vp, _vp, _vp, _d, _i, ctypes.POINTER(_i), _dp, _vp]
     L.hpfem_plan1d.argtypes = [_dp, _i, _i, _i, _d, _vp, ctypes.POINTER(_vp)]
     L.hpfem_plan1d_info.argtypes = [_vp, ctypes.POINTER(_i)]
     L.hpfem_solve1d.argtypes = [_vp, _i, _vp, _vp, _vp]
@@ -71,7 +76,8 @@ def _load():
     L.hpfem_last_error.restype = ctypes.c_char_p
     for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
               "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
-              "hpfem_plan_profile_read", "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d"):
+              "hpfem_plan_profile_read", "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_grid",
+              "hpfem_transform", "hpfem_itransform", "hpfem_varcoef_apply", "hpfem_pcg"):
         getattr(L, f).restype = _i
     _LIB = L
     return L
@@ -80,7 +86,8 @@ def _load():
 EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
            "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
            "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error",
-           "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_plan1d_destroy")
+           "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_plan1d_destroy",
+           "hpfem_grid", "hpfem_transform", "hpfem_itransform", "hpfem_varcoef_apply", "hpfem_pcg")
 
 
 class HpfemError(RuntimeError):
@@ -221,6 +228,33 @@ def hpfem_unload(plan: int, U, C_leg, stream=None):
     _check(_load().hpfem_unload(plan, _ptr(U), _ptr(C_leg), _stream(stream)))
 
 
+def hpfem_grid(plan: int, Lx: int, Ly: int):
+    """Host grid coordinates (x[(p_x+1) n_x], y[(p_y+1) n_y])."""
+    x, y = np.empty(Lx), np.empty(Ly)
+    _check(_load().hpfem_grid(plan, x.ctypes.data_as(_dp), y.ctypes.data_as(_dp)))
+    return x, y
+
+
+def hpfem_transform(plan: int, V, C, stream=None):
+    _check(_load().hpfem_transform(plan, _ptr(V), _ptr(C), _stream(stream)))
+
+
+def hpfem_itransform(plan: int, C, V, stream=None):
+    _check(_load().hpfem_itransform(plan, _ptr(C), _ptr(V), _stream(stream)))
+
+
+def hpfem_varcoef_apply(plan: int, cgrid, U, F, stream=None):
+    _check(_load().hpfem_varcoef_apply(plan, _ptr(cgrid), _ptr(U), _ptr(F), _stream(stream)))
+
+
+def hpfem_pcg(plan: int, cgrid, G, U, rtol: float, maxit: int, stream=None):
+    """Returns (iterations, relative residual)."""
+    it, rel = _i(0), _d(0.0)
+    _check(_load().hpfem_pcg(plan, _ptr(cgrid), _ptr(G), _ptr(U), rtol, maxit, ctypes.byref(it), ctypes.byref(rel),
+                             _stream(stream)))
+    return it.value, rel.value
+
+
 def hpfem_plan_launches(plan: int) -> int:
     n = ctypes.c_longlong(0)
     _check(_load().hpfem_plan_launches(plan, ctypes.byref(n)))
@@ -286,6 +320,21 @@ class Plan:
 
     def unload(self, U, C_leg, stream=None):
         hpfem_unload(self.handle, U, C_leg, stream)
+
+    def grid(self):
+        return hpfem_grid(self.handle, (self.px + 1) * self.nx, (self.py + 1) * self.ny)
+
+    def transform(self, V, C, stream=None):
+        hpfem_transform(self.handle, V, C, stream)
+
+    def itransform(self, C, V, stream=None):
+        hpfem_itransform(self.handle, C, V, stream)
+
+    def varcoef_apply(self, cgrid, U, F, stream=None):
+        hpfem_varcoef_apply(self.handle, cgrid, U, F, stream)
+
+    def pcg(self, cgrid, G, U, rtol=1e-8, maxit=200, stream=None):
+        return hpfem_pcg(self.handle, cgrid, G, U, rtol, maxit, stream)
 
     def profile(self, capacity: int):
         hpfem_plan_profile(self.handle, capacity)

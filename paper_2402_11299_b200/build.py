@@ -1,7 +1,7 @@
 """Compile the in-tree shared library libhpfem_b200.so for sm_100a.
 
   g++  -O2 -std=gnu++17   csrc/plan.cpp     (host plan, binary128 shifts)
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo  csrc/kernels.cu, tma_step.cu, solve1d.cu
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo  csrc/kernels.cu, tma_step.cu, solve1d.cu, varcoef.cu
   nvcc -shared ... -lquadmath  ->  paper_2402_11299_b200/libhpfem_b200.so
 
 nvcc cross-compiles without a GPU, so this runs on the CPU build box too.
@@ -39,6 +39,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     kern_o = os.path.join(OBJ, "kernels.o")
     tma_o = os.path.join(OBJ, "tma_step.o")
     s1d_o = os.path.join(OBJ, "solve1d.o")
+    vc_o = os.path.join(OBJ, "varcoef.o")
     out = None if verbose else subprocess.DEVNULL
     if force or _stale(plan_o, [os.path.join(CSRC, "plan.cpp")] + headers):
         subprocess.check_call(["g++", *CXX_FLAGS, "-c", os.path.join(CSRC, "plan.cpp"), "-o", plan_o])
@@ -57,9 +58,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with open(log, "w") as fh:
             subprocess.check_call([NVCC, *NVCC_FLAGS, "-c", os.path.join(CSRC, "solve1d.cu"), "-o", s1d_o],
                                   stdout=fh, stderr=subprocess.STDOUT)
-    if force or _stale(LIB, [plan_o, kern_o, tma_o, s1d_o]):
+    if force or _stale(vc_o, [os.path.join(CSRC, "varcoef.cu")] + headers):
+        log = os.path.join(OBJ, "ptxas_vc.log")
+        with open(log, "w") as fh:
+            subprocess.check_call([NVCC, *NVCC_FLAGS, "-c", os.path.join(CSRC, "varcoef.cu"), "-o", vc_o],
+                                  stdout=fh, stderr=subprocess.STDOUT)
+    if force or _stale(LIB, [plan_o, kern_o, tma_o, s1d_o, vc_o]):
         tmp = LIB + f".tmp{os.getpid()}"
-        subprocess.check_call([NVCC, "-shared", *ARCH, plan_o, kern_o, tma_o, s1d_o, "-o", tmp, "-lquadmath"],
+        subprocess.check_call([NVCC, "-shared", *ARCH, plan_o, kern_o, tma_o, s1d_o, vc_o, "-o", tmp, "-lquadmath"],
                               stdout=out)
         os.replace(tmp, LIB)
     return LIB

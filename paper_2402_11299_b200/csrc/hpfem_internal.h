@@ -153,10 +153,34 @@ cudaError_t launch_finalize(const DirDev& x, const DirDev& y, const Layout& L, c
                             const double* X, double* U, cudaStream_t st);
 cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const double* U, double* F,
                            cudaStream_t st);
-cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st);
+/* accumulate = 1: G += load(Fleg) (the variable-coefficient operator adds
+ * its Hadamard term onto hpfem_apply's output) */
+cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st,
+                          int accumulate = 0);
 cudaError_t launch_solve1d(const DirDev& d, const FacView& f, int nrhs, const double* F, double* U,
                            cudaStream_t st);  // solve1d.cu
 cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, double* Cleg, cudaStream_t st);
+
+/* NEXT-3 (varcoef.cu): one 1D pass of a grid <-> Legendre transform,
+ *   out[base(c) + k s] = [g[same]] * sum_i A[k K + i] in[base(c) + i s],
+ *   base(c) = (c / nb) bs + c % nb,  c < ncols,  k < M,  i < K. */
+struct ElemApply {
+  const double* A;
+  int M, K;
+  const double* in;
+  double* out;
+  const double* g;  // optional Hadamard factor at the output address (null = none)
+  long long ncols, nb, bs, s;
+};
+enum { CG_RZ = 0, CG_A = 1, CG_B = 2, CG_RRV = 3, CG_NSC = 4 };      // device scalar slots
+enum { CG_RZ0 = 0, CG_ALPHA = 1, CG_RR = 2, CG_BETA = 3 };            // k_cg_scalar ops
+constexpr int CG_BLOCKS = 296;                                       // 2 x 148 SMs
+cudaError_t launch_elem_apply(const ElemApply& E, cudaStream_t st);
+cudaError_t launch_dot(const double* a, const double* b, size_t n, double* partial, double* sc, int op,
+                       cudaStream_t st);
+cudaError_t launch_cg_xr(double* x, double* r, const double* p, const double* q, size_t n, double* partial,
+                         double* sc, cudaStream_t st);
+cudaError_t launch_cg_p(double* p, const double* z, size_t n, const double* sc, int first, cudaStream_t st);
 
 }  // namespace hpfem
 

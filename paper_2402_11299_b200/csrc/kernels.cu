@@ -1085,7 +1085,7 @@ __device__ __forceinline__ int load_sources(const DirDev& o, int l, int* r, doub
 }
 
 __global__ void __launch_bounds__(128) k_load2d(DirDev x, DirDev y, const double* __restrict__ Fl,
-                                                 double* __restrict__ G) {
+                                                 double* __restrict__ G, int accumulate) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   if (j >= y.N) return;
@@ -1104,6 +1104,7 @@ __global__ void __launch_bounds__(128) k_load2d(DirDev x, DirDev y, const double
       if (ry[b] >= 0) t += wy[b] * __ldg(Fl + (size_t)rx[a] * ldl + ry[b]);
     acc += wx[a] * t;
   }
+  if (accumulate) acc += G[(size_t)i * y.N + j];
   G[(size_t)i * y.N + j] = acc;
 }
 
@@ -1163,9 +1164,10 @@ cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, d
   return cudaGetLastError();
 }
 
-cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st) {
+cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st,
+                          int accumulate) {
   dim3 grid((y.N + 127) / 128, x.N);
-  k_load2d<<<grid, 128, 0, st>>>(x, y, Fleg, G);
+  k_load2d<<<grid, 128, 0, st>>>(x, y, Fleg, G, accumulate);
   return cudaGetLastError();
 }
 

@@ -308,13 +308,21 @@ struct hpfem_plan_s {
   int ev_used = 0;
   struct Rec { int kind, e0, e1; double bytes; };
   std::vector<Rec> recs;
+  // NEXT-3 (transforms / variable coefficient / PCG), allocated on first use
+  double* d_tr = nullptr;         // [T_x | V_x | T_y | V_y], (p+1)^2 each: F_p and F_p^{-1}
+  double* gs0 = nullptr;          // two L_x x L_y grid / coefficient scratch arrays
+  double* gs1 = nullptr;
+  double* cg = nullptr;           // PCG vectors r | z | p | q (N_x N_y each)
+  double* cg_part = nullptr;      // reduction partials [CG_BLOCKS]
+  double* cg_sc = nullptr;        // device scalars [CG_NSC]
+  double* h_sc = nullptr;         // pinned host copy of one scalar
 };
 
 namespace {
 
-int count_launch(hpfem_plan_t pl, cudaError_t e, const char* where) {
+int count_launch(hpfem_plan_t pl, cudaError_t e, const char* where, int kernels = 1) {
   if (e != cudaSuccess) return cuda_err(e, where);
-  ++pl->launches;
+  pl->launches += kernels;
   return HPFEM_OK;
 }
 
@@ -362,6 +370,13 @@ void free_plan(hpfem_plan_t pl) {
   cudaFree(pl->d_err);
   cudaFree(pl->wx);
   cudaFree(pl->wy);
+  cudaFree(pl->d_tr);
+  cudaFree(pl->gs0);
+  cudaFree(pl->gs1);
+  cudaFree(pl->cg);
+  cudaFree(pl->cg_part);
+  cudaFree(pl->cg_sc);
+  if (pl->h_sc) cudaFreeHost(pl->h_sc);
   delete pl;
 }
 
@@ -860,6 +875,268 @@ int hpfem_unload(hpfem_plan_t pl, const double* U, double* C_leg, void* cuda_str
   const int rc = count_launch(pl, launch_unload2d(pl->dx, pl->dy, U, C_leg, st), "unload");
   prof_add(pl, 3, e0, prof_mark(pl, st), (double)bl + (double)bu);
   return rc;
+}
+
+/* ---------------- NEXT-3: transforms, variable coefficient, PCG ---------------- */
+}  // extern "C"
+
+namespace {
+
+typedef long double ld_t;
+
+/* reference points x_i = cos(pi (2i + 1) / (2m)), i = 0..m-1, m = p + 1: the
+ * paper's first-kind Chebyshev points sin(pi (m - 2k + 1)/(2m)), k = i + 1
+ * (reading R17), descending */
+ld_t cheb_theta(int i, int m) { return 3.14159265358979323846264338327950288L * (2 * i + 1) / (2.0L * m); }
+
+/* Legendre P_0..P_p at x (Bonnet recurrence) */
+void legendre_all(ld_t x, int p, ld_t* P) {
+  P[0] = 1.0L;
+  if (p >= 1) P[1] = x;
+  for (int k = 1; k < p; ++k) P[k + 1] = ((2 * k + 1) * x * P[k] - k * P[k - 1]) / (k + 1);
+}
+
+/* Gauss-Legendre nodes and weights (Newton on P_m) */
+void gauss_legendre(int m, std::vector<ld_t>& x, std::vector<ld_t>& w) {
+  x.resize(m);
+  w.resize(m);
+  std::vector<ld_t> P(m + 1);
+  for (int i = 0; i < m; ++i) {
+    ld_t z = cosl(3.14159265358979323846264338327950288L * (i + 0.75L) / (m + 0.5L)), dp = 0;
+    for (int it = 0; it < 100; ++it) {
+      legendre_all(z, m, P.data());
+      dp = m * (z * P[m] - P[m - 1]) / (z * z - 1.0L);
+      const ld_t dz = P[m] / dp;
+      z -= dz;
+      if (fabsl(dz) < 1e-19L) break;
+    }
+    legendre_all(z, m, P.data());
+    dp = m * (z * P[m] - P[m - 1]) / (z * z - 1.0L);
+    x[i] = z;
+    w[i] = 2.0L / ((1.0L - z * z) * dp * dp);
+  }
+}
+
+/* T = F_p (values at the m = p + 1 points -> Legendre coefficients) as the
+ * product of the DCT-II (values -> Chebyshev coefficients of the
+ * interpolant, a_j = (2 - delta_j0)/m sum_i f_i cos(j theta_i)) with the
+ * Chebyshev -> Legendre conversion L[k][j] = (k + 1/2) int P_k T_j (Gauss-
+ * Legendre, m nodes: exact for k + j <= 2m - 1), the construction of
+ * P:L904-L908; V = F_p^{-1}, V[i][k] = P_k(x_i).  Row-major (p+1)^2, extended
+ * precision, rounded once. */
+void transform_matrices(int p, double* T, double* V) {
+  const int m = p + 1;
+  std::vector<ld_t> gx, gw, P(m + 1), L((size_t)m * m, 0.0L), D((size_t)m * m);
+  gauss_legendre(m, gx, gw);
+  for (int q = 0; q < m; ++q) {
+    legendre_all(gx[q], p, P.data());
+    const ld_t th = acosl(gx[q]);
+    for (int j = 0; j < m; ++j) {
+      const ld_t Tj = cosl(j * th);
+      for (int k = 0; k < m; ++k) L[(size_t)k * m + j] += (k + 0.5L) * gw[q] * P[k] * Tj;
+    }
+  }
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < m; ++i) D[(size_t)j * m + i] = (j == 0 ? 1.0L : 2.0L) / m * cosl(j * cheb_theta(i, m));
+  for (int k = 0; k < m; ++k)
+    for (int i = 0; i < m; ++i) {
+      ld_t acc = 0;
+      for (int j = 0; j < m; ++j) acc += L[(size_t)k * m + j] * D[(size_t)j * m + i];
+      T[(size_t)k * m + i] = (double)acc;
+    }
+  for (int i = 0; i < m; ++i) {
+    legendre_all(cosl(cheb_theta(i, m)), p, P.data());
+    for (int k = 0; k < m; ++k) V[(size_t)i * m + k] = (double)P[k];
+  }
+}
+
+size_t leg_elems(const hpfem_plan_t pl) { return (size_t)(pl->hx.p + 1) * pl->hx.n * (pl->hy.p + 1) * pl->hy.n; }
+
+int ensure_transforms(hpfem_plan_t pl, cudaStream_t st) {
+  if (pl->d_tr) return HPFEM_OK;
+  const int mx = pl->hx.p + 1, my = pl->hy.p + 1;
+  std::vector<double> h((size_t)2 * mx * mx + (size_t)2 * my * my);
+  transform_matrices(pl->hx.p, h.data(), h.data() + (size_t)mx * mx);
+  transform_matrices(pl->hy.p, h.data() + (size_t)2 * mx * mx, h.data() + (size_t)2 * mx * mx + (size_t)my * my);
+  cudaError_t ce;
+  const size_t gb = sizeof(double) * leg_elems(pl);
+  if ((ce = cudaMalloc(&pl->d_tr, sizeof(double) * h.size())) != cudaSuccess ||
+      (ce = cudaMalloc(&pl->gs0, gb)) != cudaSuccess || (ce = cudaMalloc(&pl->gs1, gb)) != cudaSuccess) {
+    cudaFree(pl->d_tr);
+    cudaFree(pl->gs0);
+    pl->d_tr = pl->gs0 = nullptr;
+    return ce == cudaErrorMemoryAllocation ? set_err(HPFEM_ENOMEM, "transform buffers: out of device memory")
+                                           : cuda_err(ce, "transform buffers");
+  }
+  if ((ce = cudaMemcpyAsync(pl->d_tr, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st)) !=
+      cudaSuccess)
+    return cuda_err(ce, "transform upload");
+  return cudaStreamSynchronize(st) == cudaSuccess ? HPFEM_OK : cuda_err(cudaGetLastError(), "transform upload");
+}
+
+/* the two 1D passes of one 2D transform; inverse = 0: values -> coefficients
+ * (F_x . F_y^T), 1: coefficients -> values, times g if given */
+int transform2d(hpfem_plan_t pl, int inverse, const double* in, double* tmp, double* out, const double* g,
+                cudaStream_t st) {
+  const int mx = pl->hx.p + 1, my = pl->hy.p + 1, nx = pl->hx.n, ny = pl->hy.n;
+  const long long Lx = (long long)mx * nx, Ly = (long long)my * ny;
+  const double* Ax = pl->d_tr + (inverse ? (size_t)mx * mx : 0);
+  const double* Ay = pl->d_tr + (size_t)2 * mx * mx + (inverse ? (size_t)my * my : 0);
+  ElemApply E{};
+  E.A = Ax; E.M = mx; E.K = mx; E.in = in; E.out = tmp; E.g = nullptr;
+  E.ncols = (long long)nx * Ly; E.nb = E.ncols; E.bs = 0; E.s = (long long)nx * Ly;
+  int rc = count_launch(pl, launch_elem_apply(E, st), "transform x");
+  if (rc) return rc;
+  E.A = Ay; E.M = my; E.K = my; E.in = tmp; E.out = out; E.g = g;
+  E.ncols = Lx * ny; E.nb = ny; E.bs = Ly; E.s = ny;
+  return count_launch(pl, launch_elem_apply(E, st), "transform y");
+}
+
+/* F = A_x U M_y + M_x U A_y + <v, c u>, the last by eq. (evaluation) */
+int varcoef_core(hpfem_plan_t pl, const double* cgrid, const double* U, double* F, cudaStream_t st) {
+  int rc;
+  if ((rc = count_launch(pl, launch_apply2d(pl->dx, pl->dy, pl->omega, U, F, st), "apply"))) return rc;
+  if ((rc = count_launch(pl, launch_unload2d(pl->dx, pl->dy, U, pl->gs0, st), "unload"))) return rc;
+  if ((rc = transform2d(pl, 1, pl->gs0, pl->gs1, pl->gs0, cgrid, st))) return rc;  // c o values
+  if ((rc = transform2d(pl, 0, pl->gs0, pl->gs1, pl->gs0, nullptr, st))) return rc;
+  return count_launch(pl, launch_load2d(pl->dx, pl->dy, pl->gs0, F, st, 1), "load (accumulate)");
+}
+
+bool overlap_n(const void* a, size_t na, const void* b, size_t nb) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + nb && y < x + na;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hpfem_grid(hpfem_plan_t pl, double* x, double* y) {
+  t_err.clear();
+  if (!pl || !x || !y) return set_err(HPFEM_EINVAL, "null argument");
+  for (int d = 0; d < 2; ++d) {
+    const DirHost& h = d == 0 ? pl->hx : pl->hy;
+    double* out = d == 0 ? x : y;
+    const int m = h.p + 1;
+    for (int i = 0; i < m; ++i) {
+      const ld_t t = cosl(cheb_theta(i, m));
+      for (int e = 0; e < h.n; ++e)
+        out[(size_t)i * h.n + e] = (double)((ld_t)h.xs[e] + (t + 1.0L) * ((ld_t)h.xs[e + 1] - (ld_t)h.xs[e]) / 2.0L);
+    }
+  }
+  return HPFEM_OK;
+}
+
+int hpfem_transform(hpfem_plan_t pl, const double* V, double* C, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !V || !C) return set_err(HPFEM_EINVAL, "null argument");
+  const size_t b = sizeof(double) * leg_elems(pl);
+  if (overlap_n(V, b, C, b)) return set_err(HPFEM_EINVAL, "V and C overlap");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  pl->launches = 0;
+  int rc = ensure_transforms(pl, st);
+  if (rc) return rc;
+  return transform2d(pl, 0, V, pl->gs0, C, nullptr, st);
+}
+
+int hpfem_itransform(hpfem_plan_t pl, const double* C, double* V, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !V || !C) return set_err(HPFEM_EINVAL, "null argument");
+  const size_t b = sizeof(double) * leg_elems(pl);
+  if (overlap_n(V, b, C, b)) return set_err(HPFEM_EINVAL, "C and V overlap");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  pl->launches = 0;
+  int rc = ensure_transforms(pl, st);
+  if (rc) return rc;
+  return transform2d(pl, 1, C, pl->gs0, V, nullptr, st);
+}
+
+int hpfem_varcoef_apply(hpfem_plan_t pl, const double* cgrid, const double* U, double* F, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !cgrid || !U || !F) return set_err(HPFEM_EINVAL, "null argument");
+  const size_t bn = sizeof(double) * (size_t)pl->hx.N * pl->hy.N, bl = sizeof(double) * leg_elems(pl);
+  if (overlap_n(U, bn, F, bn) || overlap_n(cgrid, bl, F, bn)) return set_err(HPFEM_EINVAL, "F overlaps an input");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  pl->launches = 0;
+  int rc = ensure_transforms(pl, st);
+  if (rc) return rc;
+  return varcoef_core(pl, cgrid, U, F, st);
+}
+
+int hpfem_pcg(hpfem_plan_t pl, const double* cgrid, const double* G, double* U, double rtol, int maxit, int* iters,
+              double* relres, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !cgrid || !G || !U) return set_err(HPFEM_EINVAL, "null argument");
+  if (!(rtol >= 0.0) || maxit < 0) return set_err(HPFEM_EINVAL, "rtol < 0 or maxit < 0");
+  const size_t nn = (size_t)pl->hx.N * pl->hy.N, bn = sizeof(double) * nn, bl = sizeof(double) * leg_elems(pl);
+  if (overlap_n(G, bn, U, bn) || overlap_n(cgrid, bl, U, bn)) return set_err(HPFEM_EINVAL, "U overlaps an input");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  long long launches = 0;
+  pl->launches = 0;
+  int rc = ensure_transforms(pl, st);
+  if (rc) return rc;
+  cudaError_t ce;
+  if (!pl->cg) {
+    if ((ce = cudaMalloc(&pl->cg, 4 * bn)) != cudaSuccess || (ce = cudaMalloc(&pl->cg_part, sizeof(double) * CG_BLOCKS)) != cudaSuccess ||
+        (ce = cudaMalloc(&pl->cg_sc, sizeof(double) * CG_NSC)) != cudaSuccess ||
+        (ce = cudaMallocHost(&pl->h_sc, sizeof(double))) != cudaSuccess) {
+      cudaFree(pl->cg);
+      cudaFree(pl->cg_part);
+      cudaFree(pl->cg_sc);
+      pl->cg = pl->cg_part = pl->cg_sc = nullptr;
+      pl->h_sc = nullptr;
+      return ce == cudaErrorMemoryAllocation ? set_err(HPFEM_ENOMEM, "pcg buffers: out of device memory")
+                                             : cuda_err(ce, "pcg buffers");
+    }
+  }
+  double *r = pl->cg, *z = r + nn, *p = z + nn, *q = p + nn;
+  auto read_rr = [&](double& v) {
+    if ((ce = cudaMemcpyAsync(pl->h_sc, pl->cg_sc + CG_RRV, sizeof(double), cudaMemcpyDeviceToHost, st)) !=
+            cudaSuccess ||
+        (ce = cudaStreamSynchronize(st)) != cudaSuccess)
+      return cuda_err(ce, "pcg residual");
+    v = *pl->h_sc;
+    return (int)HPFEM_OK;
+  };
+  auto step = [&](int r_) {
+    launches += pl->launches;
+    pl->launches = 0;
+    return r_;
+  };
+  if ((ce = cudaMemsetAsync(U, 0, bn, st)) != cudaSuccess) return cuda_err(ce, "pcg init");
+  if ((ce = cudaMemcpyAsync(r, G, bn, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return cuda_err(ce, "pcg init");
+  if ((rc = count_launch(pl, launch_dot(G, G, nn, pl->cg_part, pl->cg_sc, CG_RR, st), "pcg dot", 2))) return rc;
+  double bb = 0.0;
+  if ((rc = read_rr(bb))) return rc;
+  const double nb = std::sqrt(bb);
+  int it = 0;
+  double rel = nb > 0.0 ? 1.0 : 0.0;
+  if (nb > 0.0) {
+    if ((rc = step(solve_core(pl, pl->ws, r, z, pl->J, st)))) return rc;  // z = P r (ADI)
+    if ((rc = count_launch(pl, launch_dot(r, z, nn, pl->cg_part, pl->cg_sc, CG_RZ0, st), "pcg dot", 2))) return rc;
+    if ((rc = count_launch(pl, launch_cg_p(p, z, nn, pl->cg_sc, 1, st), "pcg p"))) return rc;
+    while (it < maxit) {
+      if ((rc = step(varcoef_core(pl, cgrid, p, q, st)))) return rc;  // q = A p
+      if ((rc = count_launch(pl, launch_dot(p, q, nn, pl->cg_part, pl->cg_sc, CG_ALPHA, st), "pcg dot", 2)))
+        return rc;
+      if ((rc = count_launch(pl, launch_cg_xr(U, r, p, q, nn, pl->cg_part, pl->cg_sc, st), "pcg update", 2)))
+        return rc;
+      ++it;
+      double rr = 0.0;
+      if ((rc = read_rr(rr))) return rc;
+      rel = std::sqrt(rr) / nb;
+      if (!std::isfinite(rel)) return set_err(HPFEM_ENUMERIC, "pcg: non-finite residual");
+      if (rel <= rtol) break;
+      if ((rc = step(solve_core(pl, pl->ws, r, z, pl->J, st)))) return rc;
+      if ((rc = count_launch(pl, launch_dot(r, z, nn, pl->cg_part, pl->cg_sc, CG_BETA, st), "pcg dot", 2))) return rc;
+      if ((rc = count_launch(pl, launch_cg_p(p, z, nn, pl->cg_sc, 0, st), "pcg p"))) return rc;
+    }
+  }
+  pl->launches += launches;
+  if (iters) *iters = it;
+  if (relres) *relres = rel;
+  return HPFEM_OK;
 }
 
 /* ---------------- 1D solver workload (NEXT-2, the paper's Fig. 1) ---------------- */
