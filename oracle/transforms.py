@@ -84,7 +84,7 @@ def itransform(px: int, nx: int, py: int, ny: int, C) -> np.ndarray:
 def coefficient_grid(xs, px, ys, py, fun) -> np.ndarray:
     """G = [g(x_k, y_j)] on the tensor grid."""
     gx, gy = grid_1d(xs, px), grid_1d(ys, py)
-    return np.ascontiguousarray(np.broadcast_to(fun(gx[:, None], gy[None, :]), (gx.size, gy.size)), dtype=np.float64)
+    return np.array(np.broadcast_to(fun(gx[:, None], gy[None, :]), (gx.size, gy.size)), dtype=np.float64)
 
 
 def varcoef_apply(xs, px, ys, py, bc, cgrid, U, omega=0.0) -> np.ndarray:
