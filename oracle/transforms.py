@@ -143,3 +143,99 @@ def graded_mesh_Tm(m: int) -> np.ndarray:
     of eq. (graded-mesh)."""
     pos = [10.0 ** (-j) for j in range(m, 0, -1)]
     return np.array([-1.0] + [-v for v in reversed(pos)] + [0.0] + pos + [1.0])
+
+
+# ------------------------------------------------------------------ NEXT-4
+def unload_matrix_1d(xs, p: int, bc: int) -> np.ndarray:
+    """Dense R ((p+1) n x N): Legendre coefficients of the hat/bubble
+    expansion, W_k = (P_k - P_{k+2})/(2k+3) (eq. app:1, P:L1074), hats
+    (1 -+ t)/2 = P_0/2 -+ P_1/2 (P:L1082)."""
+    from . import dim
+
+    xs = np.asarray(xs, dtype=np.float64)
+    n = xs.size - 1
+    N = dim(n, p, bc)
+    dl, dr = bc in (0, 2), bc in (0, 3)
+    nh = n + 1 - dl - dr
+    R = np.zeros(((p + 1) * n, N))
+    for e in range(n):
+        for side, node in ((0, e), (1, e + 1)):
+            if (node == 0 and dl) or (node == n and dr):
+                continue
+            h = node - (1 if dl else 0)
+            R[e, h] += 0.5
+            R[n + e, h] += -0.5 if side == 0 else 0.5
+        for k in range(p - 1):
+            R[k * n + e, nh + k * n + e] += 1.0 / (2 * k + 3)
+            R[(k + 2) * n + e, nh + k * n + e] += -1.0 / (2 * k + 3)
+    return R
+
+
+def deriv_matrix_1d(xs, p: int, bc: int) -> np.ndarray:
+    """Dense D ((p+1) n x N): Legendre coefficients of du/dx.  On an element
+    of width delta, dx = (delta/2) dt, W_k' = -P_{k+1} and the hats
+    (1 -+ t)/2 have slopes -+ 1/delta."""
+    from . import dim
+
+    xs = np.asarray(xs, dtype=np.float64)
+    n = xs.size - 1
+    N = dim(n, p, bc)
+    dl, dr = bc in (0, 2), bc in (0, 3)
+    nh = n + 1 - dl - dr
+    D = np.zeros(((p + 1) * n, N))
+    for e in range(n):
+        d = xs[e + 1] - xs[e]
+        for side, node in ((0, e), (1, e + 1)):
+            if (node == 0 and dl) or (node == n and dr):
+                continue
+            D[e, node - (1 if dl else 0)] += (-1.0 if side == 0 else 1.0) / d
+        for k in range(p - 1):
+            D[(k + 1) * n + e, nh + k * n + e] += -2.0 / d
+    return D
+
+
+def deriv_unload(xs, px, ys, py, bc, U) -> np.ndarray:
+    """Legendre coefficients of du/dx: D_x U R_y^T."""
+    from . import split_bc
+
+    bx, by = split_bc(bc)
+    return deriv_matrix_1d(xs, px, bx) @ np.asarray(U, dtype=np.float64) @ unload_matrix_1d(ys, py, by).T
+
+
+def explicit_step(xs, px, ys, py, dt, W) -> np.ndarray:
+    """Nonlinear half-step of the IMEX scheme on the
+    grid: U_{k+1} = F [V - dt V_x o V] with V = F^{-1} R W R^T F^{-T} and
+    V_x = F^{-1} D W R^T F^{-T}.  The sign is that of the PDE
+    u_t + u u_x = eps Delta u (the listing prints '+', reading
+    R21).  Zero Dirichlet ends."""
+    from . import unload
+
+    xs, ys = np.asarray(xs, dtype=np.float64), np.asarray(ys, dtype=np.float64)
+    nx, ny = xs.size - 1, ys.size - 1
+    V = itransform(px, nx, py, ny, unload(xs, px, ys, py, 0, W))
+    Vx = itransform(px, nx, py, ny, deriv_unload(xs, px, ys, py, 0, W))
+    return transform(px, nx, py, ny, V - dt * (Vx * V))
+
+
+def imex_step(xs, px, ys, py, eps, dt, tol, Uleg) -> np.ndarray:
+    """One step of u_t + u u_x = eps Delta u, zero Dirichlet:
+    implicit Euler u_{k+1/2} = (I - dt eps Delta)^{-1} u_k as the screened
+    problem (K(x)M + M(x)K + w^2 M(x)M) W = w^2 <v, u_k>, w = 1/sqrt(dt eps),
+    by ADI (Alg. 2), then explicit_step.  Uleg: piecewise Legendre
+    coefficients (the F_leg layout)."""
+    from . import adi_solve, load
+
+    w = 1.0 / np.sqrt(dt * eps)
+    G = load(xs, px, ys, py, 0, Uleg) * (w * w)
+    W, _ = adi_solve(xs, px, ys, py, w, 0, tol, G)
+    return explicit_step(xs, px, ys, py, dt, W)
+
+
+def legendre_l2_sq(xs, px, ys, py, C) -> float:
+    """||u||^2_{L2} of a piecewise tensor Legendre expansion (||P_k||^2 =
+    2/(2k+1), scaled by delta/2 per direction)."""
+    xs, ys = np.asarray(xs, dtype=np.float64), np.asarray(ys, dtype=np.float64)
+    nx, ny = xs.size - 1, ys.size - 1
+    wx = np.array([(xs[e + 1] - xs[e]) / (2 * k + 1) for k in range(px + 1) for e in range(nx)])
+    wy = np.array([(ys[e + 1] - ys[e]) / (2 * k + 1) for k in range(py + 1) for e in range(ny)])
+    return float(np.einsum("i,j,ij->", wx, wy, np.asarray(C) ** 2))

@@ -156,3 +156,88 @@ def test_table1_iteration_counts(m, p):
     xs, b, cg = table1_problem(m, p)
     U, it, hist = T.pcg(xs, p, xs, p, 0, cg, b, rtol=g["rtol"], tol_pre=g["adi_tol"])
     assert it == g["iters"][str(m)][str(p)], (m, p, it, hist)
+
+
+# ------------------------------------------------------------------ NEXT-4
+@pytest.mark.parametrize("bc", [0, 1, 2, 3])
+def test_unload_matrix_matches_oracle_unload(bc):
+    """The dense 1D R of the IMEX oracle equals the C++ oracle's unload
+    (itself pinned against the Jacobi-defined basis)."""
+    xs = rand_mesh(4, seed=bc)
+    p = 6
+    N = oracle.dim(4, p, bc)
+    U = RNG.standard_normal((N, 1))
+    ys = np.array([-1.0, 1.0])
+    R = T.unload_matrix_1d(xs, p, bc)
+    C = oracle.unload(xs, p, ys, 2, oracle.bc2d(bc, 0), np.hstack([U]))  # y: one Dirichlet element, one bubble
+    np.testing.assert_allclose(R @ U[:, 0] * (1.0 / 3.0), C[:, 0], atol=1e-14)
+
+
+def test_derivative_unload_is_legder():
+    """D_x U R_y^T = the per-element Legendre derivative
+    (numpy legder, times 2/delta) of the unloaded expansion."""
+    xs, ys = rand_mesh(3, seed=11), rand_mesh(2, 0, 1, seed=12)
+    px, py = 7, 5
+    U = RNG.standard_normal((oracle.dim(3, px, 0), oracle.dim(2, py, 0)))
+    C = oracle.unload(xs, px, ys, py, 0, U)
+    Cx = T.deriv_unload(xs, px, ys, py, 0, U)
+    for e in range(3):
+        ref = npleg.legder(C[e::3, :], axis=0) * 2.0 / (xs[e + 1] - xs[e])
+        np.testing.assert_allclose(Cx[e::3, :][:px], ref, atol=1e-12 * np.abs(ref).max())
+        assert np.all(Cx[px * 3 + e, :] == 0.0)
+
+
+def test_explicit_step_pointwise():
+    """itransform(explicit_step(W)) = u - dt u u_x at every grid point, with u
+    and u_x evaluated directly (numpy legval2d / legder on each element)."""
+    xs, ys = rand_mesh(2, seed=13), rand_mesh(3, seed=14)
+    px, py, dt = 6, 5, 0.05
+    W = RNG.standard_normal((oracle.dim(2, px, 0), oracle.dim(3, py, 0)))
+    Y = T.itransform(px, 2, py, 3, T.explicit_step(xs, px, ys, py, dt, W))
+    C = oracle.unload(xs, px, ys, py, 0, W)
+    gx, gy = T.grid_1d(xs, px), T.grid_1d(ys, py)
+    for i in range(0, gx.size, 2):
+        for j in range(0, gy.size, 2):
+            u = _eval_2d(xs, px, ys, py, C, gx[i], gy[j])
+            ex = min(np.searchsorted(xs, gx[i], side="right") - 1, 1)
+            Cd = np.zeros_like(C)
+            for e in range(2):
+                Cd[e::2, :][:px] = npleg.legder(C[e::2, :], axis=0) * 2.0 / (xs[e + 1] - xs[e])
+            ux = _eval_2d(xs, px, ys, py, Cd, gx[i], gy[j])
+            assert abs(Y[i, j] - (u - dt * u * ux)) <= 1e-11 * (1 + abs(u) * (1 + abs(ux))), (i, j, ex)
+
+
+def test_imex_linear_limit_heat_decay():
+    """Amplitude 1e-10: the nonlinear term is dt |u_x| ~ 3e-12 relative, so one step
+    is implicit Euler for the heat equation, whose exact action on the
+    eigenfunction sin(pi x) sin(pi y) of (-1,1)^2 is division by
+    1 + 2 pi^2 dt eps; p = 16 resolves it to ~1e-12."""
+    xs = ys = np.linspace(-1, 1, 3)
+    p, eps, dt, a = 16, 0.1, 0.01, 1e-10
+    u0 = lambda x, y: a * np.sin(np.pi * x) * np.sin(np.pi * y)
+    U0 = T.transform(p, 2, p, 2, T.coefficient_grid(xs, p, ys, p, u0))
+    U1 = T.imex_step(xs, p, ys, p, eps, dt, 1e-13, U0)
+    ref = U0 / (1 + 2 * np.pi ** 2 * dt * eps)
+    err = np.sqrt(T.legendre_l2_sq(xs, p, ys, p, U1 - ref) / T.legendre_l2_sq(xs, p, ys, p, ref))
+    assert err <= 1e-9, err
+
+
+def test_imex_energy_decays_discontinuous_data():
+    """Burgers with zero Dirichlet data dissipates: d/dt ||u||^2 =
+    -2 eps ||grad u||^2 (the convective term is skew).  Piecewise constant
+    initial data on 9 x 9 elements of (-1,1)^2 (the Fig. 'discont' setting,
+    P:L780: 'resolve the right-hand side exactly'), eps = 0.1 (Fig. burgers
+    caption)."""
+    xs = ys = np.linspace(-1, 1, 10)
+    p, eps, dt = 6, 0.1, 1e-3
+    vals = np.random.default_rng(3).standard_normal((9, 9))
+    U = np.zeros(((p + 1) * 9, (p + 1) * 9))
+    U[:9, :9] = vals
+    e0 = T.legendre_l2_sq(xs, p, ys, p, U)
+    prev = e0
+    for _ in range(4):
+        U = T.imex_step(xs, p, ys, p, eps, dt, 1e-10, U)
+        e = T.legendre_l2_sq(xs, p, ys, p, U)
+        assert e < prev
+        prev = e
+    assert prev < 0.99 * e0
