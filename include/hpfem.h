@@ -4,7 +4,7 @@
  *
  * Problem (eq. poisson):  -Laplace(u) + w^2 u = f  on
  * [a,b] x [c,d] with zero Dirichlet (basis Q) or zero Neumann
- * (basis C) conditions on all four sides, discretised in the
+ * (basis C) conditions, per side (HPFEM_BC_*), discretised in the
  * hat + integrated-Legendre (Babuska-Suri) basis of P:L138-L184 and solved
  * as the generalised Sylvester equation (eq. 2d:poisson P:L419-L424 /
  * eq. adi:poisson P:L658-L664)
@@ -18,9 +18,9 @@
  * Layout of every 2D array (U, F, G): fp64, N_x x N_y, row-major, contiguous
  * (leading dimension N_y); row i = x-dof, column j = y-dof.  Within each
  * dimension the dofs are ordered degree-major / element-minor as in
- * the kept hats first (n-1 for Dirichlet, n+1 for Neumann), then
- * for k = 0..p-2 the n bubbles W_{k,e}, e = 0..n-1.  N = p n - 1 (Dirichlet,
- * P:L384) or p n + 1 (Neumann).
+ * the kept hats first (n-1 for Dirichlet, n+1 for Neumann, n for
+ * mixed ends), then for k = 0..p-2 the n bubbles W_{k,e}, e = 0..n-1.  N =
+ * p n - 1 (Dirichlet), p n + 1 (Neumann) or p n (mixed).
  *
  * Ownership: the caller owns F, U, F_leg (DEVICE pointers, e.g. torch
  * tensors).  The plan owns its factor tables, shift tables, stencil-weight
@@ -195,6 +195,26 @@ int hpfem_itransform(hpfem_plan_t plan, const double* C, double* V, void* cuda_s
 int hpfem_varcoef_apply(hpfem_plan_t plan, const double* cgrid, const double* U, double* F, void* cuda_stream);
 int hpfem_pcg(hpfem_plan_t plan, const double* cgrid, const double* G, double* U, double rtol, int maxit, int* iters,
               double* relres, void* cuda_stream);
+
+/*
+ * hpfem_imex_step -- one implicit-explicit time step of the viscous Burgers
+ * equation u_t + u u_x = eps Delta u, zero Dirichlet data (NEXT-4 of SURVEY
+ * 8(f); Section 6):
+ *   u_{k+1/2} = (I - dt eps Delta)^{-1} u_k        (implicit Euler, ADI solve)
+ *   u_{k+1}   = u_{k+1/2} - dt u_{k+1/2} d/dx u_{k+1/2}   (explicit Euler on the
+ *               grid; the sign of the PDE, R21)
+ * The plan must be built with omega = 1/sqrt(dt eps) (the implicit step is
+ * the screened problem -Delta w + omega^2 w = omega^2 u_k) and Dirichlet
+ * ends in both directions; its tol is the ADI tolerance.  U_leg (in) and
+ * U_next (out): device piecewise-Legendre coefficients ((p_x+1) n_x) x
+ * ((p_y+1) n_y) (the F_leg layout); the product is formed on the grid (R17)
+ * and transformed back: U_next = F [V - dt V_x o V], V = F^{-1} R W R^T
+ * F^{-T}, V_x = F^{-1} D W R^T F^{-T}, D the derivative of the
+ * hat/bubble expansion (W_k' = -P_{k+1}).  EINVAL on dt <= 0, a plan
+ * with omega = 0, or overlapping buffers.  Uses the plan's solve workspace
+ * and scratch (not concurrently with another call on the same plan).
+ */
+int hpfem_imex_step(hpfem_plan_t plan, double dt, const double* U_leg, double* U_next, void* cuda_stream);
 
 /*
  * 1D solver workload (NEXT-2 of SURVEY 8(f); the paper's Fig. 1):

@@ -64,6 +64,7 @@ def _load():
     L.hpfem_itransform.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_varcoef_apply.argtypes = [_vp, _vp, _vp, _vp, _vp]
     L.hpfem_pcg.argtypes = [_vp, _vp, _vp, _vp, _d, _i, ctypes.POINTER(_i), _dp, _vp]
+    L.hpfem_imex_step.argtypes = [_vp, _d, _vp, _vp, _vp]
     L.hpfem_plan1d.argtypes = [_dp, _i, _i, _i, _d, _vp, ctypes.POINTER(_vp)]
     L.hpfem_plan1d_info.argtypes = [_vp, ctypes.POINTER(_i)]
     L.hpfem_solve1d.argtypes = [_vp, _i, _vp, _vp, _vp]
@@ -77,7 +78,7 @@ def _load():
     for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
               "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
               "hpfem_plan_profile_read", "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_grid",
-              "hpfem_transform", "hpfem_itransform", "hpfem_varcoef_apply", "hpfem_pcg"):
+              "hpfem_transform", "hpfem_itransform", "hpfem_varcoef_apply", "hpfem_pcg", "hpfem_imex_step"):
         getattr(L, f).restype = _i
     _LIB = L
     return L
@@ -87,7 +88,8 @@ EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shift
            "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
            "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error",
            "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_plan1d_destroy",
-           "hpfem_grid", "hpfem_transform", "hpfem_itransform", "hpfem_varcoef_apply", "hpfem_pcg")
+           "hpfem_grid", "hpfem_transform", "hpfem_itransform", "hpfem_varcoef_apply", "hpfem_pcg",
+           "hpfem_imex_step")
 
 
 class HpfemError(RuntimeError):
@@ -255,6 +257,10 @@ def hpfem_pcg(plan: int, cgrid, G, U, rtol: float, maxit: int, stream=None):
     return it.value, rel.value
 
 
+def hpfem_imex_step(plan: int, dt: float, U_leg, U_next, stream=None):
+    _check(_load().hpfem_imex_step(plan, dt, _ptr(U_leg), _ptr(U_next), _stream(stream)))
+
+
 def hpfem_plan_launches(plan: int) -> int:
     n = ctypes.c_longlong(0)
     _check(_load().hpfem_plan_launches(plan, ctypes.byref(n)))
@@ -335,6 +341,9 @@ class Plan:
 
     def pcg(self, cgrid, G, U, rtol=1e-8, maxit=200, stream=None):
         return hpfem_pcg(self.handle, cgrid, G, U, rtol, maxit, stream)
+
+    def imex_step(self, dt, U_leg, U_next, stream=None):
+        hpfem_imex_step(self.handle, dt, U_leg, U_next, stream)
 
     def profile(self, capacity: int):
         hpfem_plan_profile(self.handle, capacity)

@@ -156,13 +156,15 @@ cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const
 /* accumulate = 1: G += load(Fleg) (the variable-coefficient operator adds
  * its Hadamard term onto hpfem_apply's output) */
 cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st,
-                          int accumulate = 0);
+                          int accumulate = 0, double scale = 1.0);  // G (+)= scale * load(Fleg)
 cudaError_t launch_solve1d(const DirDev& d, const FacView& f, int nrhs, const double* F, double* U,
                            cudaStream_t st);  // solve1d.cu
-cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, double* Cleg, cudaStream_t st);
+/* dx = 1: Legendre coefficients of du/dx instead of u (NEXT-4) */
+cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, double* Cleg, cudaStream_t st,
+                            int dx = 0);
 
 /* NEXT-3 (varcoef.cu): one 1D pass of a grid <-> Legendre transform,
- *   out[base(c) + k s] = [g[same]] * sum_i A[k K + i] in[base(c) + i s],
+ *   out[base(c) + k s] = [h[o] + alpha *] [g[o] *] sum_i A[k K + i] in[base(c) + i s],
  *   base(c) = (c / nb) bs + c % nb,  c < ncols,  k < M,  i < K. */
 struct ElemApply {
   const double* A;
@@ -170,6 +172,8 @@ struct ElemApply {
   const double* in;
   double* out;
   const double* g;  // optional Hadamard factor at the output address (null = none)
+  const double* h;  // optional: out = h[o] + alpha * acc * g[o] (NEXT-4 explicit Euler step; needs g)
+  double alpha;
   long long ncols, nb, bs, s;
 };
 enum { CG_RZ = 0, CG_A = 1, CG_B = 2, CG_RRV = 3, CG_NSC = 4 };      // device scalar slots

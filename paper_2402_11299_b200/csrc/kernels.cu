@@ -1085,7 +1085,7 @@ __device__ __forceinline__ int load_sources(const DirDev& o, int l, int* r, doub
 }
 
 __global__ void __launch_bounds__(128) k_load2d(DirDev x, DirDev y, const double* __restrict__ Fl,
-                                                 double* __restrict__ G, int accumulate) {
+                                                 double* __restrict__ G, int accumulate, double scale) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   if (j >= y.N) return;
@@ -1104,6 +1104,7 @@ __global__ void __launch_bounds__(128) k_load2d(DirDev x, DirDev y, const double
       if (ry[b] >= 0) t += wy[b] * __ldg(Fl + (size_t)rx[a] * ldl + ry[b]);
     acc += wx[a] * t;
   }
+  acc *= scale;
   if (accumulate) acc += G[(size_t)i * y.N + j];
   G[(size_t)i * y.N + j] = acc;
 }
@@ -1135,6 +1136,26 @@ __device__ __forceinline__ void unload_sources(const DirDev& o, int r, int* d, d
   }
 }
 
+/* Derivative unload (NEXT-4): Legendre coefficient (degree m, element e) of
+ * du/dx as a combination of <= 2 dofs: d/dx W_k = -(2/delta) P_{k+1}
+ * (W_k' = -P_{k+1}, P:L84 with dx = delta/2 dt), d/dx (1 -+ t)/2 = -+ 1/delta. */
+__device__ __forceinline__ void dunload_sources(const DirDev& o, int r, int* d, double* w) {
+  const int n = o.n, m = r / n, e = r - m * n;
+  const double dl = o.delta[e];
+  d[0] = d[1] = d[2] = -1;
+  w[0] = w[1] = w[2] = 0.0;
+  if (m == 0) {
+    d[0] = hat_of_node(e, n, o.bc);
+    w[0] = -1.0 / dl;
+    d[1] = hat_of_node(e + 1, n, o.bc);
+    w[1] = 1.0 / dl;
+  } else if (m - 1 <= o.p - 2) {
+    d[0] = o.nh + (m - 1) * n + e;
+    w[0] = -2.0 / dl;
+  }
+}
+
+template <bool DX>
 __global__ void __launch_bounds__(128) k_unload2d(DirDev x, DirDev y, const double* __restrict__ U,
                                                    double* __restrict__ C) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1143,7 +1164,10 @@ __global__ void __launch_bounds__(128) k_unload2d(DirDev x, DirDev y, const doub
   if (s >= Ly) return;
   int dx[3], dy[3];
   double wx[3], wy[3];
-  unload_sources(x, r, dx, wx);
+  if (DX)
+    dunload_sources(x, r, dx, wx);
+  else
+    unload_sources(x, r, dx, wx);
   unload_sources(y, s, dy, wy);
   double acc = 0.0;
 #pragma unroll
@@ -1158,16 +1182,20 @@ __global__ void __launch_bounds__(128) k_unload2d(DirDev x, DirDev y, const doub
   C[(size_t)r * Ly + s] = acc;
 }
 
-cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, double* Cleg, cudaStream_t st) {
+cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, double* Cleg, cudaStream_t st,
+                            int dx) {
   dim3 grid(((y.p + 1) * y.n + 127) / 128, (x.p + 1) * x.n);
-  k_unload2d<<<grid, 128, 0, st>>>(x, y, U, Cleg);
+  if (dx)
+    k_unload2d<true><<<grid, 128, 0, st>>>(x, y, U, Cleg);
+  else
+    k_unload2d<false><<<grid, 128, 0, st>>>(x, y, U, Cleg);
   return cudaGetLastError();
 }
 
 cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st,
-                          int accumulate) {
+                          int accumulate, double scale) {
   dim3 grid((y.N + 127) / 128, x.N);
-  k_load2d<<<grid, 128, 0, st>>>(x, y, Fleg, G, accumulate);
+  k_load2d<<<grid, 128, 0, st>>>(x, y, Fleg, G, accumulate, scale);
   return cudaGetLastError();
 }
 

@@ -312,6 +312,7 @@ struct hpfem_plan_s {
   double* d_tr = nullptr;         // [T_x | V_x | T_y | V_y], (p+1)^2 each: F_p and F_p^{-1}
   double* gs0 = nullptr;          // two L_x x L_y grid / coefficient scratch arrays
   double* gs1 = nullptr;
+  double* gs2 = nullptr;          // third grid array (NEXT-4 IMEX step), allocated on first use
   double* cg = nullptr;           // PCG vectors r | z | p | q (N_x N_y each)
   double* cg_part = nullptr;      // reduction partials [CG_BLOCKS]
   double* cg_sc = nullptr;        // device scalars [CG_NSC]
@@ -373,6 +374,7 @@ void free_plan(hpfem_plan_t pl) {
   cudaFree(pl->d_tr);
   cudaFree(pl->gs0);
   cudaFree(pl->gs1);
+  cudaFree(pl->gs2);
   cudaFree(pl->cg);
   cudaFree(pl->cg_part);
   cudaFree(pl->cg_sc);
@@ -1002,6 +1004,26 @@ int varcoef_core(hpfem_plan_t pl, const double* cgrid, const double* U, double* 
   return count_launch(pl, launch_load2d(pl->dx, pl->dy, pl->gs0, F, st, 1), "load (accumulate)");
 }
 
+/* PCG / IMEX vectors: 4 N_x N_y arrays, reduction partials, device scalars */
+int ensure_vectors(hpfem_plan_t pl) {
+  if (pl->cg) return HPFEM_OK;
+  const size_t bn = sizeof(double) * (size_t)pl->hx.N * pl->hy.N;
+  cudaError_t ce;
+  if ((ce = cudaMalloc(&pl->cg, 4 * bn)) != cudaSuccess ||
+      (ce = cudaMalloc(&pl->cg_part, sizeof(double) * CG_BLOCKS)) != cudaSuccess ||
+      (ce = cudaMalloc(&pl->cg_sc, sizeof(double) * CG_NSC)) != cudaSuccess ||
+      (ce = cudaMallocHost(&pl->h_sc, sizeof(double))) != cudaSuccess) {
+    cudaFree(pl->cg);
+    cudaFree(pl->cg_part);
+    cudaFree(pl->cg_sc);
+    pl->cg = pl->cg_part = pl->cg_sc = nullptr;
+    pl->h_sc = nullptr;
+    return ce == cudaErrorMemoryAllocation ? set_err(HPFEM_ENOMEM, "vector buffers: out of device memory")
+                                           : cuda_err(ce, "vector buffers");
+  }
+  return HPFEM_OK;
+}
+
 bool overlap_n(const void* a, size_t na, const void* b, size_t nb) {
   const char* x = (const char*)a;
   const char* y = (const char*)b;
@@ -1077,19 +1099,7 @@ int hpfem_pcg(hpfem_plan_t pl, const double* cgrid, const double* G, double* U, 
   int rc = ensure_transforms(pl, st);
   if (rc) return rc;
   cudaError_t ce;
-  if (!pl->cg) {
-    if ((ce = cudaMalloc(&pl->cg, 4 * bn)) != cudaSuccess || (ce = cudaMalloc(&pl->cg_part, sizeof(double) * CG_BLOCKS)) != cudaSuccess ||
-        (ce = cudaMalloc(&pl->cg_sc, sizeof(double) * CG_NSC)) != cudaSuccess ||
-        (ce = cudaMallocHost(&pl->h_sc, sizeof(double))) != cudaSuccess) {
-      cudaFree(pl->cg);
-      cudaFree(pl->cg_part);
-      cudaFree(pl->cg_sc);
-      pl->cg = pl->cg_part = pl->cg_sc = nullptr;
-      pl->h_sc = nullptr;
-      return ce == cudaErrorMemoryAllocation ? set_err(HPFEM_ENOMEM, "pcg buffers: out of device memory")
-                                             : cuda_err(ce, "pcg buffers");
-    }
-  }
+  if ((rc = ensure_vectors(pl))) return rc;
   double *r = pl->cg, *z = r + nn, *p = z + nn, *q = p + nn;
   auto read_rr = [&](double& v) {
     if ((ce = cudaMemcpyAsync(pl->h_sc, pl->cg_sc + CG_RRV, sizeof(double), cudaMemcpyDeviceToHost, st)) !=
@@ -1137,6 +1147,61 @@ int hpfem_pcg(hpfem_plan_t pl, const double* cgrid, const double* G, double* U, 
   if (iters) *iters = it;
   if (relres) *relres = rel;
   return HPFEM_OK;
+}
+
+int hpfem_imex_step(hpfem_plan_t pl, double dt, const double* U_leg, double* U_next, void* cuda_stream) {
+  t_err.clear();
+  if (!pl || !U_leg || !U_next) return set_err(HPFEM_EINVAL, "null argument");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return set_err(HPFEM_EINVAL, "dt must be positive");
+  if (pl->omega == 0.0) return set_err(HPFEM_EINVAL, "the plan's omega must be 1/sqrt(dt eps) > 0");
+  const size_t bl = sizeof(double) * leg_elems(pl);
+  if (overlap_n(U_leg, bl, U_next, bl)) return set_err(HPFEM_EINVAL, "U_leg and U_next overlap");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  long long launches = 0;
+  pl->launches = 0;
+  int rc = ensure_transforms(pl, st);
+  if (rc) return rc;
+  if ((rc = ensure_vectors(pl))) return rc;
+  if (!pl->gs2) {
+    cudaError_t ce = cudaMalloc(&pl->gs2, bl);
+    if (ce != cudaSuccess) {
+      pl->gs2 = nullptr;
+      return ce == cudaErrorMemoryAllocation ? set_err(HPFEM_ENOMEM, "imex buffer: out of device memory")
+                                             : cuda_err(ce, "imex buffer");
+    }
+  }
+  const size_t nn = (size_t)pl->hx.N * pl->hy.N;
+  double *G = pl->cg, *W = G + nn;
+  // linear half-step (implicit Euler): (I - dt eps Delta) w = u_k in the
+  // Galerkin form (K(x)M + M(x)K + w^2 M(x)M) W = w^2 <v, u_k>, w^2 = 1/(dt eps)
+  const double w2 = pl->omega * pl->omega;
+  if ((rc = count_launch(pl, launch_load2d(pl->dx, pl->dy, U_leg, G, st, 0, w2), "imex load"))) return rc;
+  launches += pl->launches;
+  pl->launches = 0;
+  if ((rc = solve_core(pl, pl->ws, G, W, pl->J, st))) return rc;
+  launches += pl->launches;
+  pl->launches = 0;
+  // nonlinear half-step (explicit Euler, reading R21):
+  // U_{k+1} = F [V - dt V_x o V],  V = F^{-1} R W R^T F^{-T},  V_x = F^{-1} D W R^T F^{-T}
+  if ((rc = count_launch(pl, launch_unload2d(pl->dx, pl->dy, W, pl->gs0, st, 0), "imex unload"))) return rc;
+  if ((rc = transform2d(pl, 1, pl->gs0, pl->gs1, pl->gs2, nullptr, st))) return rc;  // V
+  if ((rc = count_launch(pl, launch_unload2d(pl->dx, pl->dy, W, pl->gs0, st, 1), "imex dunload"))) return rc;
+  {
+    const int mx = pl->hx.p + 1, my = pl->hy.p + 1, nx = pl->hx.n, ny = pl->hy.n;
+    const long long Lx = (long long)mx * nx, Ly = (long long)my * ny;
+    ElemApply E{};
+    E.A = pl->d_tr + (size_t)mx * mx;  // V_x (x pass of the inverse transform)
+    E.M = mx; E.K = mx; E.in = pl->gs0; E.out = pl->gs1;
+    E.ncols = (long long)nx * Ly; E.nb = E.ncols; E.bs = 0; E.s = (long long)nx * Ly;
+    if ((rc = count_launch(pl, launch_elem_apply(E, st), "imex itransform x"))) return rc;
+    E.A = pl->d_tr + (size_t)2 * mx * mx + (size_t)my * my;  // y pass, epilogue V - dt V_x o V
+    E.M = my; E.K = my; E.in = pl->gs1; E.out = pl->gs0; E.g = pl->gs2; E.h = pl->gs2; E.alpha = -dt;
+    E.ncols = Lx * ny; E.nb = ny; E.bs = Ly; E.s = ny;
+    if ((rc = count_launch(pl, launch_elem_apply(E, st), "imex itransform y"))) return rc;
+  }
+  rc = transform2d(pl, 0, pl->gs0, pl->gs1, U_next, nullptr, st);
+  pl->launches += launches;
+  return rc;
 }
 
 /* ---------------- 1D solver workload (NEXT-2, the paper's Fig. 1) ---------------- */

@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(256) k_elem_apply(ElemApply E) {
       const int k = k0 + ty * 4 + x;
       if (k >= E.M) continue;
       const long long o = bo + (long long)k * E.s;
-      E.out[o] = E.g ? acc[x][y] * __ldg(E.g + o) : acc[x][y];
+      const double v = E.g ? acc[x][y] * __ldg(E.g + o) : acc[x][y];
+      E.out[o] = E.h ? fma(E.alpha, v, __ldg(E.h + o)) : v;
     }
   }
 }

@@ -141,3 +141,43 @@ def test_pcg_edge_cases():
     with pytest.raises(hp.HpfemError):
         plan.varcoef_apply(cgd, Z, Z)
     plan.close()
+
+
+# ------------------------------------------------------------------ NEXT-4
+IMEX = [
+    # (xs, px, ys, py, eps, dt, tol)
+    (np.linspace(-1, 1, 10), 6, np.linspace(-1, 1, 10), 6, 0.1, 1e-3, 1e-10),  # Fig. 'discont' mesh, 9 x 9
+    (rmesh(3, seed=21), 12, rmesh(4, seed=22), 9, 0.05, 2e-3, 1e-12),
+    (rmesh(2, seed=23), 33, rmesh(2, seed=24), 20, 0.1, 1e-2, 1e-10),         # TMA shapes
+]
+
+
+@pytest.mark.parametrize("case", range(len(IMEX)))
+def test_imex_steps_vs_oracle(case):
+    """hpfem_imex_step (Burgers IMEX) for 3 steps from
+    piecewise-constant random data vs the oracle's imex_step, in the L2 norm
+    of the piecewise Legendre expansion (relative 1e-10)."""
+    torch = torch_cuda()
+    xs, px, ys, py, eps, dt, tol = IMEX[case]
+    nx, ny = xs.size - 1, ys.size - 1
+    w = 1.0 / np.sqrt(dt * eps)
+    plan = gpu_plan(xs, px, ys, py, w, 0, tol)
+    U = np.zeros(((px + 1) * nx, (py + 1) * ny))
+    U[:nx, :ny] = np.random.default_rng(case).standard_normal((nx, ny))
+    Ua, Ub = _dev(U), torch.empty(U.shape, dtype=torch.float64, device="cuda")
+    Uref = U
+    for step in range(3):
+        plan.imex_step(dt, Ua, Ub)
+        Ua, Ub = Ub, Ua
+        Uref = T.imex_step(xs, px, ys, py, eps, dt, tol, Uref)
+        d = T.legendre_l2_sq(xs, px, ys, py, Ua.cpu().numpy() - Uref)
+        err = np.sqrt(d / T.legendre_l2_sq(xs, px, ys, py, Uref))
+        print(f"imex case {case} step {step}: L2 rel diff {err:.2e}")
+        assert err <= 1e-10
+    import paper_2402_11299_b200 as hp
+
+    with pytest.raises(hp.HpfemError):
+        plan.imex_step(-1.0, Ua, Ub)
+    with pytest.raises(hp.HpfemError):
+        plan.imex_step(dt, Ua, Ua)
+    plan.close()
