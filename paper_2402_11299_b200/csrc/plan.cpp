@@ -317,6 +317,11 @@ struct hpfem_plan_s {
   double* cg_part = nullptr;      // reduction partials [CG_BLOCKS]
   double* cg_sc = nullptr;        // device scalars [CG_NSC]
   double* h_sc = nullptr;         // pinned host copy of one scalar
+  // CUDA graphs of whole ADI solves (launch-bound small problems), keyed by
+  // (workspace, F, U, iters); captured on a plan-owned stream, launched on the caller's
+  struct GraphEntry { const Workspace* w; const double* F; double* U; int iters; cudaGraphExec_t exec; long long launches; };
+  std::vector<GraphEntry> graphs;
+  cudaStream_t cap = nullptr;
 };
 
 namespace {
@@ -379,6 +384,8 @@ void free_plan(hpfem_plan_t pl) {
   cudaFree(pl->cg_part);
   cudaFree(pl->cg_sc);
   if (pl->h_sc) cudaFreeHost(pl->h_sc);
+  for (auto& g : pl->graphs) cudaGraphExecDestroy(g.exec);
+  if (pl->cap) cudaStreamDestroy(pl->cap);
   delete pl;
 }
 
@@ -764,6 +771,54 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
 }
 
 
+/* solve_core replayed from a CUDA graph: the whole solve (6J + 3 kernels and
+ * the side-stream fork/joins) is captured once per (workspace, F, U, iters)
+ * on a plan-owned stream and launched on `st` -- one launch instead of
+ * hundreds, which is what bounds the small configurations.  Bitwise the same
+ * kernels with the same arguments.  Not used while profiling (per-launch
+ * events) or with HPFEM_NO_GRAPH=1; at most kMaxGraphs cached. */
+static int solve_graph(hpfem_plan_t pl, const Workspace& w, const double* F, double* U, int iters,
+                       cudaStream_t st) {
+  static int no_graph = -1;
+  if (no_graph < 0) {
+    const char* v = std::getenv("HPFEM_NO_GRAPH");
+    no_graph = v && v[0] == '1' ? 1 : 0;
+  }
+  if (no_graph || !pl->ev.empty()) return solve_core(pl, w, F, U, iters, st);
+  cudaError_t ce;
+  for (auto& g : pl->graphs)
+    if (g.w == &w && g.F == F && g.U == U && g.iters == iters) {
+      if ((ce = cudaGraphLaunch(g.exec, st)) != cudaSuccess) return cuda_err(ce, "graph launch");
+      pl->launches += g.launches;
+      return HPFEM_OK;
+    }
+  if (!pl->cap && (ce = cudaStreamCreateWithFlags(&pl->cap, cudaStreamNonBlocking)) != cudaSuccess)
+    return cuda_err(ce, "capture stream");
+  if ((ce = cudaStreamBeginCapture(pl->cap, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+    return cuda_err(ce, "begin capture");
+  const long long l0 = pl->launches;
+  int rc = solve_core(pl, w, F, U, iters, pl->cap);
+  cudaGraph_t graph = nullptr;
+  ce = cudaStreamEndCapture(pl->cap, &graph);
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (ce != cudaSuccess) return cuda_err(ce, "end capture");
+  cudaGraphExec_t exec = nullptr;
+  ce = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ce != cudaSuccess) return cuda_err(ce, "graph instantiate");
+  constexpr size_t kMaxGraphs = 4;
+  if (pl->graphs.size() >= kMaxGraphs) {
+    cudaGraphExecDestroy(pl->graphs.front().exec);
+    pl->graphs.erase(pl->graphs.begin());
+  }
+  pl->graphs.push_back({&w, F, U, iters, exec, pl->launches - l0});
+  if ((ce = cudaGraphLaunch(exec, st)) != cudaSuccess) return cuda_err(ce, "graph launch");
+  return HPFEM_OK;
+}
+
 int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, void* cuda_stream) {
   t_err.clear();
   if (!pl || !F || !U) return set_err(HPFEM_EINVAL, "null argument");
@@ -776,7 +831,7 @@ int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, vo
     cudaError_t ce = cudaMemsetAsync(U, 0, bytes, st);
     return ce == cudaSuccess ? HPFEM_OK : cuda_err(ce, "memset");
   }
-  return solve_core(pl, pl->ws, F, U, iters, st);
+  return solve_graph(pl, pl->ws, F, U, iters, st);
 }
 
 int hpfem_solve_batched(hpfem_plan_t pl, int batch, const double* F, double* U, void* cuda_stream) {
@@ -1123,7 +1178,7 @@ int hpfem_pcg(hpfem_plan_t pl, const double* cgrid, const double* G, double* U, 
   int it = 0;
   double rel = nb > 0.0 ? 1.0 : 0.0;
   if (nb > 0.0) {
-    if ((rc = step(solve_core(pl, pl->ws, r, z, pl->J, st)))) return rc;  // z = P r (ADI)
+    if ((rc = step(solve_graph(pl, pl->ws, r, z, pl->J, st)))) return rc;  // z = P r (ADI)
     if ((rc = count_launch(pl, launch_dot(r, z, nn, pl->cg_part, pl->cg_sc, CG_RZ0, st), "pcg dot", 2))) return rc;
     if ((rc = count_launch(pl, launch_cg_p(p, z, nn, pl->cg_sc, 1, st), "pcg p"))) return rc;
     while (it < maxit) {
@@ -1138,7 +1193,7 @@ int hpfem_pcg(hpfem_plan_t pl, const double* cgrid, const double* G, double* U, 
       rel = std::sqrt(rr) / nb;
       if (!std::isfinite(rel)) return set_err(HPFEM_ENUMERIC, "pcg: non-finite residual");
       if (rel <= rtol) break;
-      if ((rc = step(solve_core(pl, pl->ws, r, z, pl->J, st)))) return rc;
+      if ((rc = step(solve_graph(pl, pl->ws, r, z, pl->J, st)))) return rc;
       if ((rc = count_launch(pl, launch_dot(r, z, nn, pl->cg_part, pl->cg_sc, CG_BETA, st), "pcg dot", 2))) return rc;
       if ((rc = count_launch(pl, launch_cg_p(p, z, nn, pl->cg_sc, 0, st), "pcg p"))) return rc;
     }
@@ -1178,7 +1233,7 @@ int hpfem_imex_step(hpfem_plan_t pl, double dt, const double* U_leg, double* U_n
   if ((rc = count_launch(pl, launch_load2d(pl->dx, pl->dy, U_leg, G, st, 0, w2), "imex load"))) return rc;
   launches += pl->launches;
   pl->launches = 0;
-  if ((rc = solve_core(pl, pl->ws, G, W, pl->J, st))) return rc;
+  if ((rc = solve_graph(pl, pl->ws, G, W, pl->J, st))) return rc;
   launches += pl->launches;
   pl->launches = 0;
   // nonlinear half-step (explicit Euler, reading R21):
