@@ -163,6 +163,22 @@ cudaError_t launch_solve1d(const DirDev& d, const FacView& f, int nrhs, const do
 cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, double* Cleg, cudaStream_t st,
                             int dx = 0);
 
+/* K11 (kernels.cu): whole ADI solve of one small problem per CTA in shared memory */
+struct SmallArgs {
+  DirDev x, y;
+  const double* fx;  // factor sets (plan layout), stride sx / sy doubles
+  const double* fy;
+  size_t sx, sy;
+  const double* sh;   // [kap_x | sig_x | kap_y | sig_y] (J+1 each)
+  const double* tau;  // [tau_A (J) | tau_B (J)]: apply shifts hw2 - p_j, hw2 + q_j
+  int J, iters;
+  const double* F;
+  double* U;
+};
+size_t small_smem_bytes(const DirDev& x, const DirDev& y);
+constexpr size_t SMALL_SMEM_MAX = 200 * 1024;
+cudaError_t launch_adi_small(const SmallArgs& a, int batch, cudaStream_t st);
+
 /* NEXT-3 (varcoef.cu): one 1D pass of a grid <-> Legendre transform,
  *   out[base(c) + k s] = [h[o] + alpha *] [g[o] *] sum_i A[k K + i] in[base(c) + i s],
  *   base(c) = (c / nb) bs + c % nb,  c < ncols,  k < M,  i < K. */

@@ -1053,6 +1053,163 @@ cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const
   return cudaGetLastError();
 }
 
+/* ------------------------------------------------------------------ */
+/* K11 (small problems): the whole ADI solve of one problem in one CTA, all
+ * three arrays (G, W_j, W_{j-1/2}) in shared memory -- for the
+ * configurations whose half-steps are latency-bound (config 1: 31^2 dofs,
+ * 23 KB), where the multi-kernel path spends ~9 us per kernel on almost no
+ * data.  Same algebra as the oracle's Algorithm 2 (the "plus" form, R6),
+ * with the iterate materialised after every solve (x_b = z - v_L x_hL -
+ * v_R x_hR, no deferred correction) and the 1D solves of solve1d.cu
+ * (static condensation with the factor tables of K1).  One CTA per
+ * right-hand side: hpfem_solve_batched fills the GPU with problems. */
+/* solve (kap K + sig M) along direction d for L lines of array A, entry
+ * (line l, dof) at A[l ls + dof es], in place (solve1d.cu, all CTA threads) */
+__device__ void small_line_solve(const DirDev& d, const double* __restrict__ base, double sig, int L, int ls,
+                                 int es, double* A) {
+  const int n = d.n, nh = d.nh, nb = d.nb;
+  const double* __restrict__ il = base;
+  const double* __restrict__ g = base + nb;
+  const double* __restrict__ vL = base + 2 * (size_t)nb;
+  const double* __restrict__ vR = base + 3 * (size_t)nb;
+  const double* __restrict__ ilh = base + 4 * (size_t)nb;
+  const double* __restrict__ gh = ilh + nh;
+  for (int it = threadIdx.x; it < L * 2 * n; it += blockDim.x) {  // 1. chains z = D^{-1} r_b
+    const int l = it / (2 * n), ch = it - l * 2 * n;
+    const int pi = ch / n, e = ch - pi * n;
+    const int m = chain_len(d.p, pi);
+    double* a = A + (size_t)l * ls;
+    double y = 0.0;
+    for (int c = m - 1; c >= 0; --c) {
+      const int b = (pi + 2 * c) * n + e;
+      y = (a[(nh + b) * es] - __ldg(g + b) * y) * __ldg(il + b);
+      a[(nh + b) * es] = y;
+    }
+    double z = 0.0, gp = 0.0;
+    for (int c = 0; c < m; ++c) {
+      const int b = (pi + 2 * c) * n + e;
+      z = (a[(nh + b) * es] - gp * z) * __ldg(il + b);
+      gp = __ldg(g + b);
+      a[(nh + b) * es] = z;
+    }
+  }
+  __syncthreads();
+  const bool k1 = d.p - 2 >= 1;
+  for (int it = threadIdx.x; it < L * nh; it += blockDim.x) {  // 2. hat rhs r_h - B z
+    const int l = it / nh, t = it - l * nh;
+    double* a = A + (size_t)l * ls;
+    const int node = node_of_hat(t, d.bc), eL = node - 1, eR = node;
+    double r = a[t * es];
+    if (eL >= 0) {
+      const double dl = d.delta[eL];
+      r -= s_hat_bub(sig, dl, 1, 0) * a[(nh + eL) * es];
+      if (k1) r -= s_hat_bub(sig, dl, 1, 1) * a[(nh + n + eL) * es];
+    }
+    if (eR <= n - 1) {
+      const double dr = d.delta[eR];
+      r -= s_hat_bub(sig, dr, 0, 0) * a[(nh + eR) * es];
+      if (k1) r -= s_hat_bub(sig, dr, 0, 1) * a[(nh + n + eR) * es];
+    }
+    a[t * es] = r;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < L && nh > 0; l += blockDim.x) {  // 3. hat Schur solve per line
+    double* a = A + (size_t)l * ls;
+    double y = 0.0;
+    for (int t = nh - 1; t >= 0; --t) {
+      const double w = __ldg(ilh + t);
+      y = fma(-__ldg(gh + t) * w, y, a[t * es] * w);
+      a[t * es] = y;
+    }
+    double x = 0.0;
+    for (int t = 0; t < nh; ++t) {
+      const double w = __ldg(ilh + t);
+      x = fma(-(t > 0 ? __ldg(gh + t - 1) : 0.0) * w, x, a[t * es] * w);
+      a[t * es] = x;
+    }
+  }
+  __syncthreads();
+  for (int it = threadIdx.x; it < L * nb; it += blockDim.x) {  // 4. x_b = z - v_L x_hL - v_R x_hR
+    const int l = it / nb, b = it - l * nb;
+    const int e = b % n;
+    double* a = A + (size_t)l * ls;
+    const int hl = hat_of_node(e, n, d.bc), hr = hat_of_node(e + 1, n, d.bc);
+    double v = a[(nh + b) * es];
+    if (hl >= 0) v -= __ldg(vL + b) * a[hl * es];
+    if (hr >= 0) v -= __ldg(vR + b) * a[hr * es];
+    a[(nh + b) * es] = v;
+  }
+  __syncthreads();
+}
+
+/* out[l ls + d es] = G[...] + sum_s w_s(d) in[l ls + idx_s(d) es] for every
+ * line l < L and dof d < N of direction o (the -(kap K_o + tau M_o) apply) */
+__device__ void small_apply(const DirDev& o, double tau, int L, int ls, int es, const double* G, const double* in,
+                            double* out, Stencil* sst) {
+  for (int d = threadIdx.x; d < o.N; d += blockDim.x) stencil_build(o, d, ST_APPLY, 1.0, tau, nullptr, nullptr, sst[d]);
+  __syncthreads();
+  for (int it = threadIdx.x; it < L * o.N; it += blockDim.x) {
+    const int d = it % o.N, l = it / o.N;
+    const Stencil& st = sst[d];
+    double acc = G[(size_t)l * ls + (size_t)d * es];
+#pragma unroll
+    for (int q = 0; q < 7; ++q)
+      if (st.idx[q] >= 0) acc += st.w[q] * in[(size_t)l * ls + (size_t)st.idx[q] * es];
+    out[(size_t)l * ls + (size_t)d * es] = acc;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_adi_small(SmallArgs a) {
+  extern __shared__ double sm[];
+  const int Nx = a.x.N, Ny = a.y.N, nn = Nx * Ny;
+  double* G = sm;
+  double* W = G + nn;
+  double* H = W + nn;
+  Stencil* sst = reinterpret_cast<Stencil*>(H + nn);
+  const double* F = a.F + (size_t)blockIdx.x * nn;
+  for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+    G[i] = F[i];
+    W[i] = 0.0;
+  }
+  __syncthreads();
+  const int J = a.J;
+  for (int j = 0; j < a.iters; ++j) {
+    // W_{j-1/2} = (G - (A_x - p_j M_x) W_{j-1}) (A_y + p_j M_y)^{-1}: x-apply (lines = columns), y-solves (rows)
+    if (j == 0) {
+      for (int i = threadIdx.x; i < nn; i += blockDim.x) H[i] = G[i];
+      __syncthreads();
+    } else {
+      small_apply(a.x, a.tau[j], Ny, 1, Ny, G, W, H, sst);
+    }
+    small_line_solve(a.y, a.fy + a.sy * j, a.sh[3 * (J + 1) + j], Nx, Ny, 1, H);
+    // W_j = (A_x - q_j M_x)^{-1} (G - W_{j-1/2} (A_y + q_j M_y)): y-apply (rows), x-solves (columns)
+    small_apply(a.y, a.tau[J + j], Nx, Ny, 1, G, H, W, sst);
+    small_line_solve(a.x, a.fx + a.sx * j, a.sh[(J + 1) + j], Ny, 1, Ny, W);
+  }
+  // U = W_J M_y^{-1}: row-wise mass solves
+  small_line_solve(a.y, a.fy + a.sy * J, 1.0, Nx, Ny, 1, W);
+  double* U = a.U + (size_t)blockIdx.x * nn;
+  for (int i = threadIdx.x; i < nn; i += blockDim.x) U[i] = W[i];
+}
+
+size_t small_smem_bytes(const DirDev& x, const DirDev& y) {
+  const int Nmax = x.N > y.N ? x.N : y.N;
+  return sizeof(double) * 3 * (size_t)x.N * y.N + sizeof(Stencil) * (size_t)Nmax;
+}
+
+cudaError_t launch_adi_small(const SmallArgs& a, int batch, cudaStream_t st) {
+  const size_t smem = small_smem_bytes(a.x, a.y);
+  static size_t opted = 48 * 1024;
+  if (smem > opted) {
+    cudaError_t e = cudaFuncSetAttribute(k_adi_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    opted = smem;
+  }
+  k_adi_small<<<batch, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 /* K8 helper: Legendre sources of dof l: (M_P R)[(m,e), l] (App. A) */
 __device__ __forceinline__ int load_sources(const DirDev& o, int l, int* r, double* w) {
   const int n = o.n;

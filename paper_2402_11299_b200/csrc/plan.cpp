@@ -294,6 +294,7 @@ struct hpfem_plan_s {
   double* fy = nullptr;           // J+1 sets (y-solves, last = mass)
   double* d_delta = nullptr;      // [n_x | n_y]
   double* d_shift = nullptr;      // kap/sig arrays
+  double* d_tau = nullptr;        // apply shifts [hw2 - p_j | hw2 + q_j] (K11)
   int* d_err = nullptr;
   Layout lay{};                   // internal padded layout (hpfem_internal.h)
   Workspace ws;                   // buffers of hpfem_solve
@@ -373,6 +374,7 @@ void free_plan(hpfem_plan_t pl) {
   cudaFree(pl->fy);
   cudaFree(pl->d_delta);
   cudaFree(pl->d_shift);
+  cudaFree(pl->d_tau);
   cudaFree(pl->d_err);
   cudaFree(pl->wx);
   cudaFree(pl->wy);
@@ -505,6 +507,18 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   ky[J] = 0.0;
   sgy[J] = 1.0;  // C = M_y for the final W_J C^{-1}
   if ((ce = cudaMalloc(&pl->d_shift, sizeof(double) * sh.size())) != cudaSuccess) return fail_cuda(ce, "alloc");
+  {  // apply shifts of the two half-steps, as solve_core forms them (A.tau, B.tau)
+    std::vector<double> tau(2 * (size_t)J + 2, 0.0);
+    for (int j = 0; j < J; ++j) {
+      tau[j] = hw2 - pl->P[j];
+      tau[J + j] = hw2 + pl->Q[j];
+    }
+    if ((ce = cudaMalloc(&pl->d_tau, sizeof(double) * tau.size())) != cudaSuccess) return fail_cuda(ce, "alloc");
+    if ((ce = cudaMemcpyAsync(pl->d_tau, tau.data(), sizeof(double) * tau.size(), cudaMemcpyHostToDevice, st)) !=
+        cudaSuccess)
+      return fail_cuda(ce, "copy");
+    if ((ce = cudaStreamSynchronize(st)) != cudaSuccess) return fail_cuda(ce, "copy");
+  }
   if ((ce = cudaMemcpyAsync(pl->d_shift, sh.data(), sizeof(double) * sh.size(), cudaMemcpyHostToDevice, st)) !=
       cudaSuccess)
     return fail_cuda(ce, "copy");
@@ -819,6 +833,39 @@ static int solve_graph(hpfem_plan_t pl, const Workspace& w, const double* F, dou
   return HPFEM_OK;
 }
 
+/* K11: whole solve(s) in one kernel, one CTA per problem, when the three
+ * arrays fit in shared memory (HPFEM_NO_SMALL=1 disables; not while
+ * profiling, so that the per-kind profile stays the multi-kernel path's) */
+static bool small_path(hpfem_plan_t pl) {
+  const char* v = std::getenv("HPFEM_NO_SMALL");
+  if (v && v[0] == '1') return false;
+  return pl->ev.empty() && small_smem_bytes(pl->dx, pl->dy) <= SMALL_SMEM_MAX;
+}
+
+static int solve_small(hpfem_plan_t pl, int batch, const double* F, double* U, int iters, cudaStream_t st);
+
+/* a full solve of one right-hand side by whichever path hpfem_solve takes */
+static int solve_any(hpfem_plan_t pl, const double* F, double* U, cudaStream_t st) {
+  return small_path(pl) ? solve_small(pl, 1, F, U, pl->J, st) : solve_graph(pl, pl->ws, F, U, pl->J, st);
+}
+
+static int solve_small(hpfem_plan_t pl, int batch, const double* F, double* U, int iters, cudaStream_t st) {
+  SmallArgs a{};
+  a.x = pl->dx;
+  a.y = pl->dy;
+  a.fx = pl->fx;
+  a.fy = pl->fy;
+  a.sx = pl->sx;
+  a.sy = pl->sy;
+  a.sh = pl->d_shift;
+  a.tau = pl->d_tau;
+  a.J = pl->J;
+  a.iters = iters;
+  a.F = F;
+  a.U = U;
+  return count_launch(pl, launch_adi_small(a, batch, st), "small ADI kernel");
+}
+
 int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, void* cuda_stream) {
   t_err.clear();
   if (!pl || !F || !U) return set_err(HPFEM_EINVAL, "null argument");
@@ -831,6 +878,7 @@ int hpfem_solve_iters(hpfem_plan_t pl, const double* F, double* U, int iters, vo
     cudaError_t ce = cudaMemsetAsync(U, 0, bytes, st);
     return ce == cudaSuccess ? HPFEM_OK : cuda_err(ce, "memset");
   }
+  if (small_path(pl)) return solve_small(pl, 1, F, U, iters, st);
   return solve_graph(pl, pl->ws, F, U, iters, st);
 }
 
@@ -844,6 +892,7 @@ int hpfem_solve_batched(hpfem_plan_t pl, int batch, const double* F, double* U, 
   pl->launches = 0;
   if (batch == 0) return HPFEM_OK;
   if (!pl->ev.empty()) return set_err(HPFEM_EINVAL, "profiling is on: batched solves run on several streams");
+  if (small_path(pl)) return solve_small(pl, batch, F, U, pl->J, st);  // one CTA per problem
   int slots = batch;
   {
     const char* v = std::getenv("HPFEM_BATCH_STREAMS");
@@ -1178,7 +1227,7 @@ int hpfem_pcg(hpfem_plan_t pl, const double* cgrid, const double* G, double* U, 
   int it = 0;
   double rel = nb > 0.0 ? 1.0 : 0.0;
   if (nb > 0.0) {
-    if ((rc = step(solve_graph(pl, pl->ws, r, z, pl->J, st)))) return rc;  // z = P r (ADI)
+    if ((rc = step(solve_any(pl, r, z, st)))) return rc;  // z = P r (ADI)
     if ((rc = count_launch(pl, launch_dot(r, z, nn, pl->cg_part, pl->cg_sc, CG_RZ0, st), "pcg dot", 2))) return rc;
     if ((rc = count_launch(pl, launch_cg_p(p, z, nn, pl->cg_sc, 1, st), "pcg p"))) return rc;
     while (it < maxit) {
@@ -1193,7 +1242,7 @@ int hpfem_pcg(hpfem_plan_t pl, const double* cgrid, const double* G, double* U, 
       rel = std::sqrt(rr) / nb;
       if (!std::isfinite(rel)) return set_err(HPFEM_ENUMERIC, "pcg: non-finite residual");
       if (rel <= rtol) break;
-      if ((rc = step(solve_graph(pl, pl->ws, r, z, pl->J, st)))) return rc;
+      if ((rc = step(solve_any(pl, r, z, st)))) return rc;
       if ((rc = count_launch(pl, launch_dot(r, z, nn, pl->cg_part, pl->cg_sc, CG_BETA, st), "pcg dot", 2))) return rc;
       if ((rc = count_launch(pl, launch_cg_p(p, z, nn, pl->cg_sc, 0, st), "pcg p"))) return rc;
     }
@@ -1233,7 +1282,7 @@ int hpfem_imex_step(hpfem_plan_t pl, double dt, const double* U_leg, double* U_n
   if ((rc = count_launch(pl, launch_load2d(pl->dx, pl->dy, U_leg, G, st, 0, w2), "imex load"))) return rc;
   launches += pl->launches;
   pl->launches = 0;
-  if ((rc = solve_graph(pl, pl->ws, G, W, pl->J, st))) return rc;
+  if ((rc = solve_any(pl, G, W, st))) return rc;
   launches += pl->launches;
   pl->launches = 0;
   // nonlinear half-step (explicit Euler, reading R21):

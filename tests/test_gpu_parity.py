@@ -51,14 +51,18 @@ SMALL = [
 MIXED = list(range(12, len(SMALL)))
 
 
-@pytest.fixture(params=["tma", "ldg"])
+@pytest.fixture(params=["small", "tma", "ldg"])
 def kernel_path(request, monkeypatch):
-    """Run with the TMA half-step kernels (default) and with the LDG kernels
-    (HPFEM_NO_TMA=1, also the fallback for shapes TMA cannot express)."""
+    """Run with the one-CTA-per-problem kernel K11 (default for problems whose
+    arrays fit in shared memory), with the TMA half-step kernels
+    (HPFEM_NO_SMALL=1, the default for larger problems) and with the LDG
+    kernels (HPFEM_NO_TMA=1, also the fallback for shapes TMA cannot express)."""
+    monkeypatch.delenv("HPFEM_NO_TMA", raising=False)
+    monkeypatch.delenv("HPFEM_NO_SMALL", raising=False)
+    if request.param != "small":
+        monkeypatch.setenv("HPFEM_NO_SMALL", "1")
     if request.param == "ldg":
         monkeypatch.setenv("HPFEM_NO_TMA", "1")
-    else:
-        monkeypatch.delenv("HPFEM_NO_TMA", raising=False)
     return request.param
 
 
