@@ -70,6 +70,8 @@ def _declare(L):
     L.oracle_apply.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _dp, _dp]
     L.oracle_load.argtypes = [_dp, _i, _i, _dp, _i, _i, _i, _dp, _dp]
     L.oracle_unload.argtypes = [_dp, _i, _i, _dp, _i, _i, _i, _dp, _dp]
+    L.oracle_set_robin.argtypes = [_dp]
+    L.oracle_set_robin.restype = None
     for f in ("oracle_operator_dense", "oracle_operator_coo", "oracle_factor_dense", "oracle_solve1d",
               "oracle_spectrum", "oracle_shifts", "oracle_plan", "oracle_adi_solve", "oracle_apply", "oracle_load", "oracle_unload"):
         getattr(L, f).restype = _i
@@ -97,6 +99,24 @@ def _f64(a):
 def threads():
     """OpenMP threads used by the oracle's line loops."""
     return lib().oracle_threads()
+
+
+class robin:
+    """Context manager: Robin coefficients alpha >= 0 at (x = a, x = b,
+    y = c, y = d) for the oracle calls inside the block (the
+    1D functions use the first two).  Ends with alpha != 0 must keep their
+    hat (a Neumann end of the 1D code)."""
+
+    def __init__(self, alpha4):
+        self.a = np.ascontiguousarray(alpha4, dtype=np.float64)
+
+    def __enter__(self):
+        lib().oracle_set_robin(_ptr(self.a))
+        return self
+
+    def __exit__(self, *exc):
+        lib().oracle_set_robin(None)
+        return False
 
 
 def bc2d(bx, by):

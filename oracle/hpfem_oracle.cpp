@@ -56,6 +56,7 @@ struct Space {
                            // 2 = Dirichlet left / Neumann right, 3 = Neumann left / Dirichlet right
                            // (mixed: the hat keep/drop mask of P:L430-L435, NEXT-1 of SURVEY 8(f))
   std::vector<double> x;   // breakpoints x_0 < ... < x_n
+  double rob[2] = {0.0, 0.0};  // Robin alpha at the left / right end (0 = none)
 
   // a Dirichlet end drops its boundary hat (Q drops h_0 and h_n; C keeps all)
   bool drop_left() const { return bc == 0 || bc == 2; }
@@ -73,7 +74,7 @@ struct Space {
   double delta(int e) const { return x[e + 1] - x[e]; }
 };
 
-Space make_space(const double* xs, int n, int p, int bc) {
+Space make_space(const double* xs, int n, int p, int bc, const double* rob = nullptr) {
   if (n < 1) throw std::invalid_argument("n < 1");
   if (p < 2) throw std::invalid_argument("p < 2");
   if (bc < 0 || bc > 3) throw std::invalid_argument("bc");
@@ -84,6 +85,14 @@ Space make_space(const double* xs, int n, int p, int bc) {
   s.x.assign(xs, xs + n + 1);
   for (int e = 0; e < n; ++e)
     if (!(s.x[e + 1] > s.x[e])) throw std::invalid_argument("breakpoints not increasing");
+  if (rob) {
+    for (int side = 0; side < 2; ++side) {
+      if (!(rob[side] >= 0.0) || !std::isfinite(rob[side])) throw std::invalid_argument("Robin alpha < 0");
+      if (rob[side] != 0.0 && (side == 0 ? s.drop_left() : s.drop_right()))
+        throw std::invalid_argument("Robin alpha on a Dirichlet end");
+      s.rob[side] = rob[side];
+    }
+  }
   return s;
 }
 
@@ -181,6 +190,11 @@ void assemble(const Space& s, SpMat& K, SpMat& M) {
       }
     }
   }
+  // Robin ends: alpha <v, u>_{boundary} adds alpha h(x_end)^2 =
+  // alpha to the diagonal of the end's (kept) hat; in 2D this is the
+  // alpha <v,u>_{L2(side)} term of the tensor-product form
+  if (s.rob[0] != 0.0) K[s.hat(0)][s.hat(0)] += s.rob[0];
+  if (s.rob[1] != 0.0) K[s.hat(s.n)][s.hat(s.n)] += s.rob[1];
 }
 
 /* Entrywise combination X_ij = alpha * P_ij + beta * Q_ij over the union
@@ -407,6 +421,13 @@ bool is_spd(const Ops1D& o, double sigma) {
   return factor_b3(o.s, S, F, nullptr);
 }
 
+/* A - sigma M SPD  <=>  sigma < lambda_min (Robin ends, reading R22) */
+bool is_spd_low(const Ops1D& o, double sigma) {
+  SpMat S = combine(1.0, o.A, -sigma, o.M);
+  Factor F;
+  return factor_b3(o.s, S, F, nullptr);
+}
+
 void spectrum(const Ops1D& o, double omega, double lam[2]) {
   const Space& s = o.s;
   const double pi = 3.14159265358979323846;
@@ -414,6 +435,22 @@ void spectrum(const Ops1D& o, double omega, double lam[2]) {
   // closed-form lower bounds of the continuous spectrum (reading R4): Dirichlet
   // pi^2/L^2, Neumann 0, mixed Dirichlet/Neumann pi^2/(4 L^2) (quarter wave)
   lam[0] = (s.bc == 0 ? pi * pi / (L * L) : s.bc == 1 ? 0.0 : pi * pi / (4.0 * L * L)) + omega * omega / 2.0;
+  if (s.rob[0] != 0.0 || s.rob[1] != 0.0) {
+    // Robin ends (reading R22): no closed form; bisection on "A - sigma M is
+    // SPD" from the valid lower bound w^2/2 (K + alpha terms is PSD), keeping
+    // the SPD-confirmed lower end
+    double lo = omega * omega / 2.0, hi = std::max(2.0 * lo, 1.0);
+    int g = 0;
+    while (is_spd_low(o, hi) && g++ < 200) {
+      lo = hi;
+      hi *= 2.0;
+    }
+    while (hi - lo > 1e-13 * hi) {
+      const double mid = 0.5 * (lo + hi);
+      if (is_spd_low(o, mid)) lo = mid; else hi = mid;
+    }
+    lam[0] = lo;
+  }
   // initial upper bracket: Lemma 5.2, lambda^{-1} <= (24p^4 + w^2 h^2)/(2h^2)
   double h = s.delta(0);
   for (int e = 1; e < s.n; ++e) h = std::min(h, s.delta(e));
@@ -621,14 +658,20 @@ void split_bc(int bc, int& bx, int& by) {
   }
 }
 
+/* Robin alphas (x-left, x-right, y-left, y-right) of the next calls
+ * (oracle_set_robin; zeros = none) */
+double g_robin[4] = {0.0, 0.0, 0.0, 0.0};
+
 int make_problem(const double* xs, int nx, int px, const double* ys, int ny, int py, double omega, int bc,
                  double tol, Problem& P) {
   int bx, by;
   split_bc(bc, bx, by);
-  if ((bx == 1 || by == 1) && omega == 0.0) throw std::invalid_argument("Neumann requires omega != 0 (P:L812)");
+  const bool sx = bx == 1 && g_robin[0] == 0.0 && g_robin[1] == 0.0;  // pure Neumann: singular K
+  const bool sy = by == 1 && g_robin[2] == 0.0 && g_robin[3] == 0.0;
+  if ((sx || sy) && omega == 0.0) throw std::invalid_argument("Neumann requires omega != 0 (P:L812)");
   if (!(tol > 0.0 && tol < 1.0)) throw std::invalid_argument("tol not in (0,1)");
-  P.ox = make_ops(make_space(xs, nx, px, bx), omega);
-  P.oy = make_ops(make_space(ys, ny, py, by), omega);
+  P.ox = make_ops(make_space(xs, nx, px, bx, g_robin), omega);
+  P.oy = make_ops(make_space(ys, ny, py, by, g_robin + 2), omega);
   P.omega = omega;
   P.tol = tol;
   return 0;
@@ -643,6 +686,13 @@ extern "C" {
 
 const char* oracle_last_error(void) { return g_err.c_str(); }
 
+/* Robin coefficients alpha >= 0 at (x = a, x = b, y = c, y = d) for the
+ * following calls (alpha u + du/dn = 0); all zero = none.  The
+ * 1D functions use the first two. */
+void oracle_set_robin(const double* alpha4) {
+  for (int k = 0; k < 4; ++k) g_robin[k] = alpha4 ? alpha4[k] : 0.0;
+}
+
 /* OpenMP threads the oracle's line loops use (bench.py cpu_baseline.cores) */
 int oracle_threads(void) { return omp_get_max_threads(); }
 
@@ -655,7 +705,7 @@ int oracle_dim(int n, int p, int bc) {
 /* Dense alpha*K + beta*M (N x N, row-major) for tests on small N. */
 int oracle_operator_dense(const double* xs, int n, int p, int bc, double alpha, double beta, double* out) {
   try {
-    Space s = make_space(xs, n, p, bc);
+    Space s = make_space(xs, n, p, bc, g_robin);
     SpMat K, M;
     assemble(s, K, M);
     SpMat S = combine(alpha, K, beta, M);
@@ -673,7 +723,7 @@ int oracle_operator_dense(const double* xs, int n, int p, int bc, double alpha, 
 int oracle_operator_coo(const double* xs, int n, int p, int bc, int which, int* rows, int* cols, double* vals,
                         int* nnz) {
   try {
-    Space s = make_space(xs, n, p, bc);
+    Space s = make_space(xs, n, p, bc, g_robin);
     SpMat K, M;
     assemble(s, K, M);
     const SpMat& S = which == 0 ? K : M;
@@ -699,7 +749,7 @@ int oracle_operator_coo(const double* xs, int n, int p, int bc, int which, int* 
 int oracle_factor_dense(const double* xs, int n, int p, int bc, double alpha, double beta, double* Lout,
                         int* info) {
   try {
-    Space s = make_space(xs, n, p, bc);
+    Space s = make_space(xs, n, p, bc, g_robin);
     SpMat K, M;
     assemble(s, K, M);
     SpMat S = combine(alpha, K, beta, M);
@@ -731,7 +781,7 @@ int oracle_factor_dense(const double* xs, int n, int p, int bc, double alpha, do
 int oracle_solve1d(const double* xs, int n, int p, int bc, double alpha, double beta, const double* f, double* x,
                    int nrhs) {
   try {
-    Space s = make_space(xs, n, p, bc);
+    Space s = make_space(xs, n, p, bc, g_robin);
     SpMat K, M;
     assemble(s, K, M);
     SpMat S = combine(alpha, K, beta, M);
@@ -747,8 +797,9 @@ int oracle_solve1d(const double* xs, int n, int p, int bc, double alpha, double 
 /* [lambda_min, lambda_max] of the pencil (A, M), A = K + (w^2/2) M. */
 int oracle_spectrum(const double* xs, int n, int p, int bc, double omega, double* lam) {
   try {
-    Space s = make_space(xs, n, p, bc);
-    if (bc == 1 && omega == 0.0) return fail("Neumann requires omega != 0", -1);  // (mixed ends are definite)
+    Space s = make_space(xs, n, p, bc, g_robin);
+    if (bc == 1 && omega == 0.0 && g_robin[0] == 0.0 && g_robin[1] == 0.0)
+      return fail("Neumann requires omega != 0", -1);  // (mixed and Robin ends are definite)
     Ops1D o = make_ops(s, omega);
     spectrum(o, omega, lam);
     return 0;
