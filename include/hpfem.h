@@ -92,6 +92,16 @@ int hpfem_plan(int n_x, int p_x, int n_y, int p_y, double a, double b, double c,
 int hpfem_plan_mesh(const double* xs, int n_x, int p_x, const double* ys, int n_y, int p_y, double omega, int bc,
                     double tol, void* cuda_stream, hpfem_plan_t* out);
 
+/* As hpfem_plan_mesh with Robin ends (alpha u + du/dn = 0,
+ * the boundary term alpha <v, u>_{L2(side)} added to the stiffness of the
+ * end's hat; NEXT-1 of SURVEY 8(f)).  alpha[4] >= 0 (host) at x = a, x = b,
+ * y = c, y = d; a nonzero alpha needs a kept (Neumann-coded) end -- EINVAL
+ * on a Dirichlet end.  w = 0 is allowed when no direction is Neumann at both
+ * ends with zero alphas.  lambda_min of a Robin direction is found by
+ * bisection (R22).  alpha = 0 everywhere is hpfem_plan_mesh. */
+int hpfem_plan_robin(const double* xs, int n_x, int p_x, const double* ys, int n_y, int p_y, double omega, int bc,
+                     const double* alpha, double tol, void* cuda_stream, hpfem_plan_t* out);
+
 /* Plan summary (host outputs; any pointer may be NULL). */
 int hpfem_plan_info(hpfem_plan_t plan, int* N_x, int* N_y, int* J, double* lam_x /*[2]*/, double* lam_y /*[2]*/,
                     double* gamma);

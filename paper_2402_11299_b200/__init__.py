@@ -51,6 +51,7 @@ def _load():
     L = ctypes.CDLL(LIB_PATH)
     L.hpfem_plan.argtypes = [_i, _i, _i, _i, _d, _d, _d, _d, _d, _i, _d, _vp, ctypes.POINTER(_vp)]
     L.hpfem_plan_mesh.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _d, _vp, ctypes.POINTER(_vp)]
+    L.hpfem_plan_robin.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _dp, _d, _vp, ctypes.POINTER(_vp)]
     L.hpfem_plan_info.argtypes = [_vp, _ip, _ip, _ip, _dp, _dp, _dp]
     L.hpfem_plan_shifts.argtypes = [_vp, _dp, _dp]
     L.hpfem_solve.argtypes = [_vp, _vp, _vp, _vp]
@@ -75,7 +76,7 @@ def _load():
     L.hpfem_plan_destroy.argtypes = [_vp]
     L.hpfem_plan_destroy.restype = None
     L.hpfem_last_error.restype = ctypes.c_char_p
-    for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
+    for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
               "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
               "hpfem_plan_profile_read", "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_grid",
               "hpfem_transform", "hpfem_itransform", "hpfem_varcoef_apply", "hpfem_pcg", "hpfem_imex_step"):
@@ -84,7 +85,7 @@ def _load():
     return L
 
 
-EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
+EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
            "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
            "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error",
            "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_plan1d_destroy",
@@ -133,6 +134,18 @@ def _stream(stream) -> int:
 def hpfem_plan(n_x, p_x, n_y, p_y, a, b, c, d, omega, bc, tol, stream=None) -> int:
     h = _vp()
     _check(_load().hpfem_plan(n_x, p_x, n_y, p_y, a, b, c, d, omega, bc, tol, _stream(stream), ctypes.byref(h)))
+    return h.value
+
+
+def hpfem_plan_robin(xs, p_x, ys, p_y, omega, bc, alpha, tol, stream=None) -> int:
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    ys = np.ascontiguousarray(ys, dtype=np.float64)
+    al = np.ascontiguousarray(alpha, dtype=np.float64)
+    if al.shape != (4,):
+        raise ValueError("alpha must hold 4 values (x=a, x=b, y=c, y=d)")
+    h = _vp()
+    _check(_load().hpfem_plan_robin(xs.ctypes.data_as(_dp), xs.size - 1, p_x, ys.ctypes.data_as(_dp), ys.size - 1,
+                                 p_y, omega, bc, al.ctypes.data_as(_dp), tol, _stream(stream), ctypes.byref(h)))
     return h.value
 
 
@@ -290,8 +303,11 @@ def hpfem_plan_destroy(plan: int):
 class Plan:
     """RAII wrapper: Plan(xs, px, ys, py, omega, bc, tol) or Plan.uniform(...)."""
 
-    def __init__(self, xs, px, ys, py, omega, bc, tol, stream=None):
-        self.handle = hpfem_plan_mesh(xs, px, ys, py, omega, bc, tol, stream)
+    def __init__(self, xs, px, ys, py, omega, bc, tol, stream=None, robin=None):
+        if robin is None:
+            self.handle = hpfem_plan_mesh(xs, px, ys, py, omega, bc, tol, stream)
+        else:
+            self.handle = hpfem_plan_robin(xs, px, ys, py, omega, bc, robin, tol, stream)
         info = hpfem_plan_info(self.handle)
         self.__dict__.update(info)
         self.px, self.py, self.bc, self.omega, self.tol = px, py, bc, omega, tol

@@ -20,6 +20,7 @@ struct DirDev {
   int N;     // dofs = nh + nb
   int nb;    // bubbles = (p-1) n
   const double* delta;  // device [n] element widths
+  double rob0, rob1;    // Robin alpha at the left / right end (0 = none)
 };
 
 /* Factor tables of one shifted operator S = kap K + sig M of one direction

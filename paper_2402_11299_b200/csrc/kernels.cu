@@ -144,6 +144,8 @@ __global__ void k_factor_hats(DirDev d, const double* __restrict__ kap, const do
     double diag = 0.0;
     if (eL >= 0) diag += s_hat_diag_elem(K, S, d.delta[eL]) - schur_elem(d, S, vR, eL, 1);
     if (eR <= d.n - 1) diag += s_hat_diag_elem(K, S, d.delta[eR]) - schur_elem(d, S, vL, eR, 0);
+    if (node == 0) diag += K * d.rob0;  // Robin boundary term alpha h(a)^2
+    if (node == d.n) diag += K * d.rob1;
     double gc = 0.0;
     if (t < d.nh - 1) {
       // A~0(t, t+1): element eR lies between the two nodes; t is its left hat
@@ -260,6 +262,8 @@ __device__ __forceinline__ void stencil_build(const DirDev& o, int l, int mode, 
       if (cvL) ctt -= s0 * cvL[eR] + (k1 ? s1 * cvL[n + eR] : 0.0);
       if (cvR && has_p) ctp -= s0 * cvR[eR] + (k1 ? s1 * cvR[n + eR] : 0.0);
     }
+    if (node == 0) ctt += kap * o.rob0;  // Robin boundary term
+    if (node == n) ctt += kap * o.rob1;
     st.idx[0] = t; st.w[0] = -ctt;
     if (has_m) { st.idx[1] = t - 1; st.w[1] = -ctm; }
     if (has_p) { st.idx[2] = t + 1; st.w[2] = -ctp; }

@@ -56,11 +56,16 @@ bool split_bc(int bc, int& bx, int& by) {
 /* host view of one direction */
 struct DirHost {
   int n = 0, p = 0, bc = 0, nh = 0, N = 0, nb = 0;
+  double rob[2] = {0.0, 0.0};  // Robin alpha at the left / right end
   std::vector<double> xs, delta;
 };
 
-DirHost make_dir(const double* xs, int n, int p, int bc) {
+DirHost make_dir(const double* xs, int n, int p, int bc, const double* rob = nullptr) {
   DirHost d;
+  if (rob) {
+    d.rob[0] = rob[0];
+    d.rob[1] = rob[1];
+  }
   d.n = n;
   d.p = p;
   d.bc = bc;
@@ -124,6 +129,8 @@ bool spd_host(const DirHost& d, double kap, double sig) {
     double diag = 0.0;
     if (eL >= 0) diag += s_hat_diag_elem(kap, sig, d.delta[eL]) - schur(vR, eL, 1);
     if (eR <= n - 1) diag += s_hat_diag_elem(kap, sig, d.delta[eR]) - schur(vL, eR, 0);
+    if (node == 0) diag += kap * d.rob[0];  // Robin boundary term
+    if (node == n) diag += kap * d.rob[1];
     if (t < d.nh - 1) {
       const double gc = (s_hat_off_elem(kap, sig, d.delta[eR]) - schur(vR, eR, 0)) / lnext;
       diag -= gc * gc;
@@ -151,6 +158,23 @@ void spectral_interval(const DirHost& d, double omega, double lam[2]) {
             : d.bc == HPFEM_BC_NEUMANN ? 0.0
                                        : pi * pi / (4.0 * len * len)) +
            hw2;
+  if (d.rob[0] != 0.0 || d.rob[1] != 0.0) {
+    // Robin ends (reading R22): bisection on "A - sigma M = K + (w^2/2 - sigma) M
+    // is SPD" from the valid lower bound w^2/2, keeping the SPD-confirmed end
+    double lo = hw2, hi = std::max(2.0 * lo, 1.0);
+    for (int it = 0; it < 200 && spd_host(d, 1.0, hw2 - hi); ++it) {
+      lo = hi;
+      hi *= 2.0;
+    }
+    while (hi - lo > 1e-13 * hi) {
+      const double mid = lo + 0.5 * (hi - lo);
+      if (spd_host(d, 1.0, hw2 - mid))
+        lo = mid;
+      else
+        hi = mid;
+    }
+    lam[0] = lo;
+  }
   double h = d.delta[0];
   for (double x : d.delta) h = std::min(h, x);
   const double p2 = (double)d.p * d.p;
@@ -432,7 +456,7 @@ int validate_mesh(const double* xs, int n, int p) {
 }
 
 int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int py, double omega, int bc, double tol,
-               cudaStream_t st, hpfem_plan_t* out) {
+               cudaStream_t st, hpfem_plan_t* out, const double* robin = nullptr) {
   if (!out) return set_err(HPFEM_EINVAL, "null out");
   *out = nullptr;
   int rc;
@@ -442,15 +466,26 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   if (!split_bc(bc, bx, by)) return set_err(HPFEM_EINVAL, "bad bc");
   if (!(tol > 0.0 && tol < 1.0)) return set_err(HPFEM_EINVAL, "tol must lie in (0,1)");
   if (!std::isfinite(omega)) return set_err(HPFEM_EINVAL, "omega not finite");
-  if ((bx == HPFEM_BC_NEUMANN || by == HPFEM_BC_NEUMANN) && omega == 0.0)
-    return set_err(HPFEM_EINVAL, "Neumann requires omega != 0 (P:L812)");
+  double rob[4] = {0.0, 0.0, 0.0, 0.0};
+  if (robin) {
+    for (int k = 0; k < 4; ++k) {
+      if (!(robin[k] >= 0.0) || !std::isfinite(robin[k])) return set_err(HPFEM_EINVAL, "Robin alpha < 0 or not finite");
+      const int b1 = k < 2 ? bx : by;
+      const bool dropped = (k % 2 == 0) ? drop_left(b1) : drop_right(b1);
+      if (robin[k] != 0.0 && dropped) return set_err(HPFEM_EINVAL, "Robin alpha on a Dirichlet end");
+      rob[k] = robin[k];
+    }
+  }
+  const bool sing_x = bx == HPFEM_BC_NEUMANN && rob[0] == 0.0 && rob[1] == 0.0;
+  const bool sing_y = by == HPFEM_BC_NEUMANN && rob[2] == 0.0 && rob[3] == 0.0;
+  if ((sing_x || sing_y) && omega == 0.0) return set_err(HPFEM_EINVAL, "Neumann requires omega != 0 (P:L812)");
   int ndev = 0;
   cudaError_t ce = cudaGetDeviceCount(&ndev);
   if (ce != cudaSuccess || ndev == 0) return set_err(HPFEM_ECUDA, "no CUDA device (no CPU fallback)");
 
   hpfem_plan_t pl = new hpfem_plan_s();
-  pl->hx = make_dir(xs, nx, px, bx);
-  pl->hy = make_dir(ys, ny, py, by);
+  pl->hx = make_dir(xs, nx, px, bx, rob);
+  pl->hy = make_dir(ys, ny, py, by, rob + 2);
   pl->omega = omega;
   pl->tol = tol;
   spectral_interval(pl->hx, omega, pl->lam_x);
@@ -486,6 +521,7 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   auto mkdev = [](const DirHost& h, const double* dd) {
     DirDev d;
     d.n = h.n; d.p = h.p; d.bc = h.bc; d.nh = h.nh; d.N = h.N; d.nb = h.nb; d.delta = dd;
+    d.rob0 = h.rob[0]; d.rob1 = h.rob[1];
     return d;
   };
   pl->dx = mkdev(hx, pl->d_delta);
@@ -671,6 +707,13 @@ int hpfem_plan_mesh(const double* xs, int n_x, int p_x, const double* ys, int n_
                     double tol, void* cuda_stream, hpfem_plan_t* out) {
   t_err.clear();
   return build_plan(xs, n_x, p_x, ys, n_y, p_y, omega, bc, tol, (cudaStream_t)cuda_stream, out);
+}
+
+int hpfem_plan_robin(const double* xs, int n_x, int p_x, const double* ys, int n_y, int p_y, double omega, int bc,
+                     const double* alpha, double tol, void* cuda_stream, hpfem_plan_t* out) {
+  t_err.clear();
+  if (!alpha) return set_err(HPFEM_EINVAL, "null alpha");
+  return build_plan(xs, n_x, p_x, ys, n_y, p_y, omega, bc, tol, (cudaStream_t)cuda_stream, out, alpha);
 }
 
 int hpfem_plan(int n_x, int p_x, int n_y, int p_y, double a, double b, double c, double d, double omega, int bc,

@@ -17,10 +17,10 @@ def torch_cuda():
     return torch
 
 
-def gpu_plan(xs, px, ys, py, omega, bc, tol):
+def gpu_plan(xs, px, ys, py, omega, bc, tol, robin=None):
     import paper_2402_11299_b200 as hp
 
-    return hp.Plan(xs, px, ys, py, omega, bc, tol)
+    return hp.Plan(xs, px, ys, py, omega, bc, tol, robin=robin)
 
 
 def gpu_solve(plan, G: np.ndarray, iters=None) -> np.ndarray:

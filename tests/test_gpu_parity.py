@@ -385,3 +385,81 @@ def test_solve1d_vs_oracle(case):
     print(f"1d case {case}: N={pl.N} rel err {err:.2e}")
     assert err <= 1e-11
     pl.close()
+
+
+# ---------------------------------------------------------------- Robin ends
+ROBIN = [
+    # (xs, px, ys, py, omega, bc, tol, alpha[x=a, x=b, y=c, y=d])
+    (rmesh(3, 0, 1, 31), 6, rmesh(4, 0, 2, 32), 5, 0.0, 1, 1e-12, [1.0, 2.0, 0.5, 3.0]),  # Robin all sides, w = 0
+    (rmesh(4, 0, 1, 33), 7, rmesh(3, 0, 1, 34), 8, 1.0, oracle.bc2d(1, 2), 1e-10, [0.0, 4.0, 0.0, 2.0]),
+    (W.graded_mesh(0, 1, 6, 0.6), 20, rmesh(5, 0, 1, 35), 18, 0.0, oracle.bc2d(3, 1), 1e-10, [5.0, 0.0, 1.0, 1.0]),
+    (rmesh(6, 0, 1, 36), 34, rmesh(8, 0, 2, 37), 24, 0.0, 1, 1e-12, [0.3, 0.3, 7.0, 0.0]),  # TMA shapes
+]
+
+
+@pytest.mark.parametrize("case", range(len(ROBIN)))
+def test_robin_cases(case, kernel_path):
+    """Robin ends (reading R22): J, shifts, solve, apply vs the
+    oracle on all kernel paths."""
+    xs, px, ys, py, om, bc, tol, al = ROBIN[case]
+    plan = gpu_plan(xs, px, ys, py, om, bc, tol, robin=al)
+    with oracle.robin(al):
+        ref = oracle.plan(xs, px, ys, py, om, bc, tol)
+        G = RNG.standard_normal((plan.Nx, plan.Ny))
+        Uref, J = oracle.adi_solve(xs, px, ys, py, om, bc, tol, G)
+        U = RNG.standard_normal((plan.Nx, plan.Ny))
+        Fref = oracle.apply(xs, px, ys, py, om, bc, U)
+    assert plan.J == ref["J"] == J
+    np.testing.assert_allclose(plan.lam_x, ref["lam_x"], rtol=1e-11)
+    np.testing.assert_allclose(plan.lam_y, ref["lam_y"], rtol=1e-11)
+    p, q = plan.shifts()
+    np.testing.assert_allclose(p, ref["p"], rtol=1e-10)
+    np.testing.assert_allclose(q, ref["q"], rtol=1e-10)
+    l2, plain = parity(xs, px, ys, py, bc, gpu_solve(plan, G), Uref)
+    print(f"robin case {case} [{kernel_path}]: N={plan.Nx}x{plan.Ny} J={J} L2 {l2:.2e} plain {plain:.2e}")
+    assert l2 <= L2_TOL
+    F = gpu_apply(plan, U)
+    assert np.abs(F - Fref).max() <= 1e-12 * np.abs(Fref).max()
+
+
+def test_robin_manufactured_mode():
+    """u = v(x) v(y), v = cos kx + (alpha/k) sin kx with alpha = k (1 - cos k) /
+    sin k, satisfies alpha u + du/dn = 0 on all four sides of [0,1]^2 and
+    -Delta u = 2 k^2 u: the GPU solution converges exponentially in p to
+    it (through hpfem_load / hpfem_unload)."""
+    torch = torch_cuda()
+    k = 2.0
+    al = k * (1 - np.cos(k)) / np.sin(k)
+    v = lambda x: np.cos(k * x) + al / k * np.sin(k * x)
+    xs = rmesh(3, 0, 1, 38)
+    errs = []
+    for p in (4, 8, 12):
+        tq, wq = np.polynomial.legendre.leggauss(p + 30)
+        cv = np.zeros((p + 1) * 3)
+        for e in range(3):
+            x = xs[e] + (tq + 1) * (xs[e + 1] - xs[e]) / 2
+            for m in range(p + 1):
+                cv[m * 3 + e] = (2 * m + 1) / 2 * np.sum(wq * np.polynomial.legendre.legval(tq, np.eye(m + 1)[m]) * v(x))
+        Cu = np.outer(cv, cv)
+        plan = gpu_plan(xs, p, xs, p, 0.0, 1, 1e-13, robin=[al] * 4)
+        G = gpu_load(plan, 2 * k * k * Cu)
+        C = gpu_unload(plan, gpu_solve(plan, G))
+        wts = np.array([(xs[e + 1] - xs[e]) / (2 * m + 1) for m in range(p + 1) for e in range(3)])
+        errs.append(float(np.sqrt(np.einsum("i,j,ij->", wts, wts, (C - Cu) ** 2))))
+        plan.close()
+    print("robin manufactured L2 errors", errs)
+    assert errs[1] < 1e-3 * errs[0] and errs[2] < 1e-9
+
+
+def test_robin_errors():
+    import paper_2402_11299_b200 as hp
+
+    xs = np.linspace(0, 1, 3)
+    with pytest.raises(hp.HpfemError) as e:
+        hp.Plan(xs, 4, xs, 4, 0.0, 0, 1e-10, robin=[1.0, 0, 0, 0])  # Robin on a Dirichlet end
+    assert e.value.code == hp.HPFEM_EINVAL
+    with pytest.raises(hp.HpfemError):
+        hp.Plan(xs, 4, xs, 4, 0.0, 1, 1e-10, robin=[-1.0, 1.0, 1.0, 1.0])  # alpha < 0
+    with pytest.raises(hp.HpfemError):
+        hp.Plan(xs, 4, xs, 4, 0.0, 1, 1e-10, robin=[1.0, 1.0, 0.0, 0.0])  # y pure Neumann, w = 0
+    hp.Plan(xs, 4, xs, 4, 0.0, 1, 1e-10, robin=[1.0, 0.0, 0.0, 1.0]).close()  # definite: fine
