@@ -14,7 +14,8 @@
  * over "columns" c: along x (rows i n_x + e) every (e, column) pair is a
  * column, contiguous (nb = n_x L_y, s = n_x L_y); along y every (row, e)
  * pair is one (nb = n_y, bs = L_y, s = n_y).  k_elem_apply is a shared-memory
- * tiled fp64 GEMM (64 outputs x 64 columns per CTA, 4 x 4 per thread); the
+ * tiled fp64 GEMM (48 outputs x 64 columns per CTA, 3 x 4 per thread,
+ * double-buffered chunks with register prefetch); the
  * Hadamard product with the coefficient grid is fused into the epilogue of
  * the inverse transform's second pass (P:L1005 'G o (...)').  fp64 has no
  * tcgen05 kind, so this runs on the FP64 pipes (K10).
@@ -30,62 +31,88 @@ namespace hpfem {
 
 namespace {
 
-constexpr int TK = 64;   // outputs per CTA
+constexpr int TK = 48;   // outputs per CTA (p + 1 = 129: 3 tiles, 90% used)
 constexpr int TC = 64;   // columns per CTA
 constexpr int TI = 16;   // contraction chunk
+constexpr int RK = 3;    // outputs per thread (16 thread rows x 3 = TK)
+constexpr int RC = 4;    // columns per thread (16 thread columns x 4 = TC)
 
+/* register-prefetched, double-buffered shared-memory tiles: the global loads
+ * of chunk i0 + TI are issued before the FMAs of chunk i0 */
 __global__ void __launch_bounds__(256) k_elem_apply(ElemApply E) {
-  __shared__ double As[TI][TK + 1];
-  __shared__ double Bs[TI][TC];
+  __shared__ double As[2][TI][TK + 1];
+  __shared__ double Bs[2][TI][TC];
   const int t = threadIdx.x;
   const long long c0 = (long long)blockIdx.x * TC;
   const int k0 = blockIdx.y * TK;
   const int tx = t & 15, ty = t >> 4;
-  // this thread's load column (global loads: 64 consecutive columns per i)
-  const int lc = t & 63, li = t >> 6;  // li in 0..3
+  const int lc = t & 63, li = t >> 6;  // B loads: 64 consecutive columns x 4 rows per pass
   const long long cl = c0 + lc;
   const bool lvalid = cl < E.ncols;
   const long long bl = lvalid ? (cl / E.nb) * E.bs + cl % E.nb : 0;
-  double acc[4][4];
+  double acc[RK][RC];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < RK; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  for (int i0 = 0; i0 < E.K; i0 += TI) {
-    // A chunk: As[i][k] = A[k0 + k][i0 + i]
-    for (int q = t; q < TI * TK; q += 256) {
-      const int k = q / TI, i = q % TI;
+    for (int b = 0; b < RC; ++b) acc[a][b] = 0.0;
+  constexpr int NA = (TI * TK + 255) / 256;  // A elements per thread per chunk
+  double ra[NA], rb[TI / 4];
+  auto gload = [&](int i0) {
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      const int idx = t + 256 * q;
+      const int k = idx / TI, i = idx % TI;
       const int kk = k0 + k, ii = i0 + i;
-      As[i][k] = (kk < E.M && ii < E.K) ? __ldg(E.A + (size_t)kk * E.K + ii) : 0.0;
+      ra[q] = (idx < TI * TK && kk < E.M && ii < E.K) ? __ldg(E.A + (size_t)kk * E.K + ii) : 0.0;
     }
 #pragma unroll
     for (int r = 0; r < TI / 4; ++r) {
-      const int i = li + 4 * r, ii = i0 + i;
-      Bs[i][lc] = (lvalid && ii < E.K) ? __ldg(E.in + bl + (long long)ii * E.s) : 0.0;
+      const int ii = i0 + li + 4 * r;
+      rb[r] = (lvalid && ii < E.K) ? __ldg(E.in + bl + (long long)ii * E.s) : 0.0;
     }
-    __syncthreads();
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      const int idx = t + 256 * q;
+      if (idx < TI * TK) As[buf][idx % TI][idx / TI] = ra[q];
+    }
+#pragma unroll
+    for (int r = 0; r < TI / 4; ++r) Bs[buf][li + 4 * r][lc] = rb[r];
+  };
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  int buf = 0;
+  for (int i0 = 0; i0 < E.K; i0 += TI) {
+    const bool more = i0 + TI < E.K;
+    if (more) gload(i0 + TI);
 #pragma unroll
     for (int i = 0; i < TI; ++i) {
-      double a[4], b[4];
+      double a[RK], b[RC];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = As[i][ty * 4 + r];
+      for (int r = 0; r < RK; ++r) a[r] = As[buf][i][ty * RK + r];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) b[r] = Bs[i][tx + 16 * r];
+      for (int r = 0; r < RC; ++r) b[r] = Bs[buf][i][tx + 16 * r];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < RK; ++x)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+        for (int y = 0; y < RC; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
     }
-    __syncthreads();
+    if (more) {
+      sstore(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
   }
 #pragma unroll
-  for (int y = 0; y < 4; ++y) {
+  for (int y = 0; y < RC; ++y) {
     const long long c = c0 + tx + 16 * y;
     if (c >= E.ncols) continue;
     const long long bo = (c / E.nb) * E.bs + c % E.nb;
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int k = k0 + ty * 4 + x;
+    for (int x = 0; x < RK; ++x) {
+      const int k = k0 + ty * RK + x;
       if (k >= E.M) continue;
       const long long o = bo + (long long)k * E.s;
       const double v = E.g ? acc[x][y] * __ldg(E.g + o) : acc[x][y];
