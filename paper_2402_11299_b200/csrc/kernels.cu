@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(256) k_bubbles(StepParams P) {
  * hats), then the hat tridiagonal reverse-Cholesky solve of each line from
  * shared memory, then the write-back.  smem: [nh][LB] doubles. */
 template <int DIR, int LB>
-__global__ void __launch_bounds__(256) k_hats(StepParams P) {
+__global__ void __launch_bounds__(256, 4) k_hats(StepParams P) {
   extern __shared__ double sh[];
   const DirDev& s = P.s;
   const int nh = s.nh, ld = P.ld, n = s.n;
