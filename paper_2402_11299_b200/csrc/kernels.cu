@@ -472,7 +472,16 @@ __global__ void __launch_bounds__(256) k_bubbles(StepParams P) {
 
 /* K5: hat right-hand side r_h - B z for a tile of LB lines (parallel over
  * hats), then the hat tridiagonal reverse-Cholesky solve of each line from
- * shared memory, then the write-back.  smem: [nh][LB] doubles. */
+ * shared memory, then the write-back.
+ * smem: [nh][LB] values, hat factors il/g [nh] each, the per-hat coupling
+ * coefficients B(h, W_0/W_1) of the left/right element [nh][4] (0 for an
+ * absent element, whose index is clamped to the present one so that every
+ * load is unconditional and issued ahead of the FMAs), (DIR 1) the LB row
+ * stencils, then the int tables (elements [nh][2], stencil indices [LB][7]). */
+__host__ __device__ constexpr size_t hats_smem_doubles(int nh, int LB) {
+  return (size_t)nh * (LB + 6) + 7 * (size_t)LB + ((size_t)nh * 2 + 7 * (size_t)LB + 1) / 2;
+}
+
 template <int DIR, int LB>
 __global__ void __launch_bounds__(256, 4) k_hats(StepParams P) {
   extern __shared__ double sh[];
@@ -480,40 +489,62 @@ __global__ void __launch_bounds__(256, 4) k_hats(StepParams P) {
   const int nh = s.nh, ld = P.ld, n = s.n;
   const int l0 = blockIdx.x * LB;  // first line (processing position) of the tile
   const double S = P.f.sig;
-  const bool k1 = s.p - 2 >= 1;
+  const bool k1 = s.p - 2 >= 1;  // bubble W_1 exists (uniform)
   const double* __restrict__ G = P.G;
   const double* __restrict__ Xp = P.Xp;
-  const double* __restrict__ out_r = P.out;
-  auto rhs_hat = [&](const Stencil& st, int li, int t) {
-    double rh = rhs_at<DIR>(G, P.alphaG, Xp, st, li, t, ld);
+  const double* __restrict__ out_r = P.out;  // chain-first bubbles of this half-step (read-only here)
+  double* fil = sh + (size_t)nh * LB;
+  double* fg = fil + nh;
+  double* hz = fg + nh;
+  double* stw = hz + 4 * (size_t)nh;
+  int* hzi = reinterpret_cast<int*>(stw + 7 * LB);
+  int* sti = hzi + 2 * nh;
+  // phase 0: hat factors, coupling tables, (DIR 1) row stencils
+  for (int t = threadIdx.x; t < nh; t += blockDim.x) {
+    fil[t] = __ldg(P.f.ilh + t);
+    fg[t] = __ldg(P.f.gh + t);
     const int node = node_of_hat(t, s.bc);
     const int eL = node - 1, eR = node;
-    if (DIR == 1 && P.z01) {  // chain-first bubbles from the compact copy
-      const double* zr = P.z01 + (size_t)li * 2 * n;
-      if (eL >= 0) {
-        const double dl = s.delta[eL];
-        const double2 v = *reinterpret_cast<const double2*>(zr + 2 * eL);
-        rh -= s_hat_bub(S, dl, 1, 0) * v.x;
-        if (k1) rh -= s_hat_bub(S, dl, 1, 1) * v.y;
-      }
-      if (eR <= n - 1) {
-        const double dr = s.delta[eR];
-        const double2 v = *reinterpret_cast<const double2*>(zr + 2 * eR);
-        rh -= s_hat_bub(S, dr, 0, 0) * v.x;
-        if (k1) rh -= s_hat_bub(S, dr, 0, 1) * v.y;
-      }
-      return rh;
-    }
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
     if (eL >= 0) {
       const double dl = s.delta[eL];
-      rh -= s_hat_bub(S, dl, 1, 0) * out_r[addr<DIR>(li, spos_bub<DIR>(P, 0, eL), ld)];
-      if (k1) rh -= s_hat_bub(S, dl, 1, 1) * out_r[addr<DIR>(li, spos_bub<DIR>(P, 1, eL), ld)];
+      c0 = s_hat_bub(S, dl, 1, 0);
+      if (k1) c1 = s_hat_bub(S, dl, 1, 1);
     }
     if (eR <= n - 1) {
       const double dr = s.delta[eR];
-      rh -= s_hat_bub(S, dr, 0, 0) * out_r[addr<DIR>(li, spos_bub<DIR>(P, 0, eR), ld)];
-      if (k1) rh -= s_hat_bub(S, dr, 0, 1) * out_r[addr<DIR>(li, spos_bub<DIR>(P, 1, eR), ld)];
+      c2 = s_hat_bub(S, dr, 0, 0);
+      if (k1) c3 = s_hat_bub(S, dr, 0, 1);
     }
+    hz[4 * t] = c0;
+    hz[4 * t + 1] = c1;
+    hz[4 * t + 2] = c2;
+    hz[4 * t + 3] = c3;
+    hzi[2 * t] = eL >= 0 ? eL : eR;
+    hzi[2 * t + 1] = eR <= n - 1 ? eR : eL;
+  }
+  if (DIR == 1 && (int)threadIdx.x < LB) {
+    const int lp = l0 + threadIdx.x;
+    Stencil st;
+    if (lp < P.o.N) {
+      line_stencil<DIR>(P, row_of(P.o, lp), st);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 7; ++q) { st.idx[q] = -1; st.w[q] = 0.0; }
+    }
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      sti[threadIdx.x * 7 + q] = st.idx[q];
+      stw[threadIdx.x * 7 + q] = st.w[q];
+    }
+  }
+  __syncthreads();
+  // r_h - B z, B z = c0 z0(eL) + c1 z1(eL) + c2 z0(eR) + c3 z1(eR) (same order as before)
+  auto coupling = [&](double rh, int t, double zl0, double zl1, double zr0, double zr1) {
+    rh -= hz[4 * t] * zl0;
+    if (k1) rh -= hz[4 * t + 1] * zl1;
+    rh -= hz[4 * t + 2] * zr0;
+    if (k1) rh -= hz[4 * t + 3] * zr1;
     return rh;
   };
   if (DIR == 0) {
@@ -524,27 +555,49 @@ __global__ void __launch_bounds__(256, 4) k_hats(StepParams P) {
     if (l >= 0) {
       Stencil st;
       line_stencil<DIR>(P, l, st);
-#pragma unroll 4
-      for (int t = tg; t < nh; t += ng) sh[t * LB + j] = rhs_hat(st, li, t);
+#pragma unroll 2
+      for (int t = tg; t < nh; t += ng) {
+        const int eL = hzi[2 * t], eR = hzi[2 * t + 1];
+        const double zl0 = __ldg(out_r + addr<DIR>(li, spos_bub<DIR>(P, 0, eL), ld));
+        const double zr0 = __ldg(out_r + addr<DIR>(li, spos_bub<DIR>(P, 0, eR), ld));
+        const double zl1 = k1 ? __ldg(out_r + addr<DIR>(li, spos_bub<DIR>(P, 1, eL), ld)) : 0.0;
+        const double zr1 = k1 ? __ldg(out_r + addr<DIR>(li, spos_bub<DIR>(P, 1, eR), ld)) : 0.0;
+        sh[t * LB + j] = coupling(rhs_at<DIR>(G, P.alphaG, Xp, st, li, t, ld), t, zl0, zl1, zr0, zr1);
+      }
     }
   } else {
-    // lines = rows: a warp per row, lanes over the contiguous hat columns
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int j = w; j < LB; j += nw) {
+    // lines = rows; the LB x nh (row, hat) items are spread over all threads
+    // (row-major: a warp reads contiguous hat columns of one or two rows)
+    int j = threadIdx.x / nh, t = threadIdx.x - j * nh;
+    for (; j < LB; t += blockDim.x) {
+      while (t >= nh) { t -= nh; ++j; }
+      if (j >= LB) break;
       const int lp = l0 + j;
       if (lp >= P.o.N) break;
       const int l = row_of(P.o, lp);
-      Stencil st;
-      line_stencil<DIR>(P, l, st);
-      for (int t = lane; t < nh; t += 32) sh[t * LB + j] = rhs_hat(st, l, t);
+      const int eL = hzi[2 * t], eR = hzi[2 * t + 1];
+      double zl0, zl1 = 0.0, zr0, zr1 = 0.0;
+      if (P.z01) {  // chain-first bubbles from the compact copy
+        const double* zr = P.z01 + (size_t)l * 2 * n;
+        const double2 vl = __ldg(reinterpret_cast<const double2*>(zr + 2 * eL));
+        const double2 vr = __ldg(reinterpret_cast<const double2*>(zr + 2 * eR));
+        zl0 = vl.x; zl1 = vl.y; zr0 = vr.x; zr1 = vr.y;
+      } else {
+        zl0 = __ldg(out_r + addr<DIR>(l, spos_bub<DIR>(P, 0, eL), ld));
+        zr0 = __ldg(out_r + addr<DIR>(l, spos_bub<DIR>(P, 0, eR), ld));
+        if (k1) {
+          zl1 = __ldg(out_r + addr<DIR>(l, spos_bub<DIR>(P, 1, eL), ld));
+          zr1 = __ldg(out_r + addr<DIR>(l, spos_bub<DIR>(P, 1, eR), ld));
+        }
+      }
+      double rh = P.alphaG != 0.0 ? P.alphaG * __ldg(G + addr<DIR>(l, t, ld)) : 0.0;
+      const int* si = sti + 7 * j;
+      const double* sw = stw + 7 * j;
+#pragma unroll
+      for (int q = 0; q < 7; ++q)
+        if (si[q] >= 0) rh += sw[q] * __ldg(Xp + addr<DIR>(si[q], t, ld));
+      sh[t * LB + j] = coupling(rh, t, zl0, zl1, zr0, zr1);
     }
-  }
-  // hat factors to shared memory (every solver thread reads the same entry: broadcast)
-  double* fil = sh + (size_t)nh * LB;
-  double* fg = fil + nh;
-  for (int t = threadIdx.x; t < nh; t += blockDim.x) {
-    fil[t] = __ldg(P.f.ilh + t);
-    fg[t] = __ldg(P.f.gh + t);
   }
   __syncthreads();
   // sequential tridiagonal reverse-Cholesky solve per line, in shared memory;
@@ -663,7 +716,7 @@ cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st) {
 
 template <int DIR, int LB>
 static cudaError_t launch_hats_lb(const StepParams& P, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (size_t)P.s.nh * (LB + 2);
+  const size_t smem = sizeof(double) * hats_smem_doubles(P.s.nh, LB);
   static size_t opted = 48 * 1024;
   if (smem > opted) {
     cudaError_t e = cudaFuncSetAttribute(k_hats<DIR, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -675,7 +728,8 @@ static cudaError_t launch_hats_lb(const StepParams& P, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-/* lines per CTA of the hat kernel (tuning knob HPFEM_HAT_LB_X / _Y: 8 or 32) */
+/* lines per CTA of the hat kernel (tuning knob HPFEM_HAT_LB_X / _Y: 8 or 32);
+ * fewer when the [nh][LB] tile would not fit in shared memory (many hats) */
 template <int DIR>
 static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
   static int lb = -1;
@@ -683,7 +737,10 @@ static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
     const char* v = getenv(DIR == 0 ? "HPFEM_HAT_LB_X" : "HPFEM_HAT_LB_Y");
     lb = v && *v ? atoi(v) : 32;
   }
-  return lb == 8 ? launch_hats_lb<DIR, 8>(P, st) : launch_hats_lb<DIR, 32>(P, st);
+  const size_t cap = 227 * 1024;
+  if (lb != 8 && sizeof(double) * hats_smem_doubles(P.s.nh, 32) <= cap) return launch_hats_lb<DIR, 32>(P, st);
+  if (sizeof(double) * hats_smem_doubles(P.s.nh, 8) <= cap) return launch_hats_lb<DIR, 8>(P, st);
+  return launch_hats_lb<DIR, 1>(P, st);
 }
 
 /* ------------------------------------------------------------------ */

@@ -1,6 +1,7 @@
 """Top stall-sampled SASS instructions of one kernel in an ncu report:
 python scripts/ncu_hot.py REPORT REGEX [SKIP] [N]"""
 import collections
+import re
 import csv
 import subprocess
 import sys
@@ -8,9 +9,19 @@ import sys
 rep, rx = sys.argv[1], sys.argv[2]
 skip = sys.argv[3] if len(sys.argv) > 3 else "0"
 n = int(sys.argv[4]) if len(sys.argv) > 4 else 15
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{rx}", "--launch-skip",
-                      skip, "--launch-count", "1", "--print-source", "sass"], capture_output=True, text=True).stdout
-rows = list(csv.reader(out.splitlines()))
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
+                     text=True).stdout
+# one block per profiled launch ("Kernel Name" line, header, rows); pick the
+# skip-th launch whose demangled name matches rx (ncu's own --kernel-name /
+# --launch-* filters do not apply to an imported report)
+blocks, cur = [], None
+for r in csv.reader(out.splitlines()):
+    if r and r[0] == "Kernel Name":
+        cur = [r]
+        blocks.append(cur)
+    elif cur is not None:
+        cur.append(r)
+rows = [b for b in blocks if re.search(rx, b[0][1])][int(skip)]
 print(rows[0][1][:100])
 hdr = rows[1]
 cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
