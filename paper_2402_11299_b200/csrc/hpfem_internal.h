@@ -39,7 +39,10 @@ struct DirDev {
  *                      sigma_{M-1} = -hd_{M-1}, sigma_c = -hd_c sigma_{c+1};
  *                    tau_c (c >= M):  z_c = z^_c + tau_c z_{M-1},
  *                      tau_M = -hu_M, tau_c = -hu_c tau_{c-1};
- *                  cfs = 4 chain_len(p, 0) + 2 (spreads smem banks).
+ *                  cfs = 4 roundup8(chain_len(p, 0)) + 2 (spreads smem banks); the
+ *                  positions past a chain up to the next multiple of 8 (the TMA
+ *                  stage height) hold zero factors, so a stage-padded
+ *                  recurrence step there yields exactly 0 with no select.
  * stored contiguously: [il | g | vL | vR | ilh | gh | cf], 256-byte aligned. */
 struct FacView {
   const double* il;
@@ -53,7 +56,7 @@ struct FacView {
   double kap, sig;
 };
 
-HD int fac_cfs(const DirDev& d) { return 4 * (d.p / 2) + 2; }
+HD int fac_cfs(const DirDev& d) { return 4 * ((d.p / 2 + 7) & ~7) + 2; }
 HD int chain_split(int p) { return (((p / 2 + 1) / 2) + 3) & ~3; }  // multiple of 4 (TMA stage height)
 
 HD size_t fac_cf_off(const DirDev& d) {

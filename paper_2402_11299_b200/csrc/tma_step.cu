@@ -488,8 +488,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int u = KCP - 1; u >= 0; --u) {
           const int c = KCP * sg + u;
-          const double yn = fma(-fb[4 * c + 1], yv, fb[4 * c] * rv[u]);
-          yv = c < mthr ? yn : 0.0;  // positions past this parity's chain stay 0
+          // positions past this parity's chain have zero factors (fac_cfs) and
+          // finite (zero-padded) inputs: yv stays exactly 0 there, no select
+          // on the dependent chain
+          yv = fma(-fb[4 * c + 1], yv, fb[4 * c] * rv[u]);
           ys[c] = yv;
         }
       }
@@ -522,13 +524,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int u = 0; u < KCP; ++u) {
               const int c = KCP * sg + u;
-              const double zn = fma(-fb[4 * c + 2], z, fb[4 * c] * ys[c]);
-              const bool live = valid && c < mthr;
-              z = live ? zn : z;
-              const double zv = live ? zn : 0.0;
-              o[swz((r - wr0) * EG + eo, u, py)] = zv;
-              if (sg == 0 && u == 0 && live && P.z01)  // chain-first bubble (degree py): compact copy
-                P.z01[(size_t)(x.nh + kx * x.n + e_x) * (2 * y.n) + 2 * ey + py] = zn;
+              z = fma(-fb[4 * c + 2], z, fb[4 * c] * ys[c]);  // 0 past the chain (see above)
+              o[swz((r - wr0) * EG + eo, u, py)] = valid ? z : 0.0;
+              if (sg == 0 && u == 0 && valid && c < mthr && P.z01)  // chain-first bubble (degree py): compact copy
+                P.z01[(size_t)(x.nh + kx * x.n + e_x) * (2 * y.n) + 2 * ey + py] = z;
             }
           }
         }
