@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhpfem_b200.so")
+LIB_PATH = os.environ.get("HPFEM_LIB_PATH") or os.path.join(_HERE, "libhpfem_b200.so")  # override: A/B builds only
 
 HPFEM_BC_DIRICHLET = 0
 HPFEM_BC_NEUMANN = 1

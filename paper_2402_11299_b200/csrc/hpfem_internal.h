@@ -33,12 +33,8 @@ struct DirDev {
  *                    [4c] = il_c, [4c+1] = hd_c = g_c il_c, [4c+2] = hu_c = g_{c-1} il_c,
  *                  so that each recurrence step is one dependent FMA,
  *                    y_c = il_c r_c - hd_c y_{c+1},   z_c = il_c y_c - hu_c z_{c-1},
- *                  and [4c+3] = the spike coefficient of the two-thread split
- *                  of the chain at M = ceil(chain_len(p,0)/2) (tma_step.cu):
- *                    sigma_c (c < M): y_c = y^_c + sigma_c y_M,
- *                      sigma_{M-1} = -hd_{M-1}, sigma_c = -hd_c sigma_{c+1};
- *                    tau_c (c >= M):  z_c = z^_c + tau_c z_{M-1},
- *                      tau_M = -hu_M, tau_c = -hu_c tau_{c-1};
+ *                  and [4c+3] = il_c again, so that each sweep reads its two
+ *                  factors with one 16-byte load: (il, hd) down, (hu, il) up;
  *                  cfs = 4 roundup8(chain_len(p, 0)) + 2 (spreads smem banks); the
  *                  positions past a chain up to the next multiple of 8 (the TMA
  *                  stage height) hold zero factors, so a stage-padded
@@ -57,7 +53,6 @@ struct FacView {
 };
 
 HD int fac_cfs(const DirDev& d) { return 4 * ((d.p / 2 + 7) & ~7) + 2; }
-HD int chain_split(int p) { return (((p / 2 + 1) / 2) + 3) & ~3; }  // multiple of 4 (TMA stage height)
 
 HD size_t fac_cf_off(const DirDev& d) {
   size_t s = 4 * (size_t)d.nb + 2 * (size_t)d.nh;

@@ -78,7 +78,7 @@ __global__ void k_factor_chains(DirDev d, const double* __restrict__ kap, const 
     g[b] = gc;
     lnext = l;
   }
-  {  // chain-major (il, g il, g_prev il, spike) for the TMA kernels (hpfem_internal.h)
+  {  // chain-major (il, g il, g_prev il, il) for the TMA kernels (hpfem_internal.h)
     double* cf = base + fac_cf_off(d) + (size_t)(2 * e + pi) * fac_cfs(d);
     double gprev = 0.0;
     for (int c = 0; c < m; ++c) {
@@ -86,18 +86,8 @@ __global__ void k_factor_chains(DirDev d, const double* __restrict__ kap, const 
       cf[4 * c] = il[b];
       cf[4 * c + 1] = g[b] * il[b];
       cf[4 * c + 2] = gprev * il[b];
+      cf[4 * c + 3] = il[b];
       gprev = g[b];
-    }
-    const int M = chain_split(d.p);
-    double sgm = 1.0;
-    for (int c = (M < m ? M : m) - 1; c >= 0; --c) {  // sigma, bottom part
-      sgm = -cf[4 * c + 1] * sgm;
-      cf[4 * c + 3] = sgm;
-    }
-    double tau = 1.0;
-    for (int c = M; c < m; ++c) {  // tau, top part
-      tau = -cf[4 * c + 2] * tau;
-      cf[4 * c + 3] = tau;
     }
   }
   // v_side = T^{-1} (beta e_0): the chain-first bubble is the only one

@@ -128,7 +128,10 @@ constexpr int NT = 256;    // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int KR = 8;      // x-solve: chain positions (rows) per stage
 constexpr int KCP = 8;     // y-solve: chain positions per stage (16 degrees)
-constexpr int SPB = 2;     // y-solve: chain stages per output staging buffer (one proxy fence each)
+#ifndef HPFEM_SPB
+#define HPFEM_SPB 2
+#endif
+constexpr int SPB = HPFEM_SPB;  // y-solve: chain stages per output staging buffer (one proxy fence each)
 #ifndef HPFEM_NOBUF
 #define HPFEM_NOBUF 2
 #endif
@@ -303,7 +306,8 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
         for (int kk = KR - 1; kk >= 0; --kk) {
           const int c = KR * sg + kk;
           if (c < m) {
-            yv = fma(-fb[4 * c + 1], yv, fb[4 * c] * rv[kk]);
+            const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c);  // (il, hd)
+            yv = fma(-f.y, yv, f.x * rv[kk]);
             ys[c] = yv;
           }
         }
@@ -315,7 +319,8 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
 #pragma unroll
       for (int c = 0; c < CL; ++c) {
         if (c < m) {
-          z = fma(-fb[4 * c + 2], z, fb[4 * c] * ys[c]);
+          const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c + 2);  // (hu, il)
+          z = fma(-f.x, z, f.y * ys[c]);
           out[(size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld] = z;
         }
       }
@@ -491,7 +496,8 @@ __global__ void __launch_bounds__(NT, 1)
           // positions past this parity's chain have zero factors (fac_cfs) and
           // finite (zero-padded) inputs: yv stays exactly 0 there, no select
           // on the dependent chain
-          yv = fma(-fb[4 * c + 1], yv, fb[4 * c] * rv[u]);
+          const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c);  // (il, hd)
+          yv = fma(-f.y, yv, f.x * rv[u]);
           ys[c] = yv;
         }
       }
@@ -524,7 +530,8 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int u = 0; u < KCP; ++u) {
               const int c = KCP * sg + u;
-              z = fma(-fb[4 * c + 2], z, fb[4 * c] * ys[c]);  // 0 past the chain (see above)
+              const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c + 2);  // (hu, il)
+              z = fma(-f.x, z, f.y * ys[c]);  // 0 past the chain (see above)
               o[swz((r - wr0) * EG + eo, u, py)] = valid ? z : 0.0;
               if (sg == 0 && u == 0 && valid && c < mthr && P.z01)  // chain-first bubble (degree py): compact copy
                 P.z01[(size_t)(x.nh + kx * x.n + e_x) * (2 * y.n) + 2 * ey + py] = z;
