@@ -21,6 +21,8 @@ struct DirDev {
   int nb;    // bubbles = (p-1) n
   const double* delta;  // device [n] element widths
   double rob0, rob1;    // Robin alpha at the left / right end (0 = none)
+  const double* lw;     // device [N][4] load weights of each dof (k_load_tab), nullptr = computed inline
+  const int* lr;        // device [N][4] their Legendre rows (-1 = none)
 };
 
 /* Factor tables of one shifted operator S = kap K + sig M of one direction
@@ -98,11 +100,15 @@ struct Layout {
 
 inline Layout make_layout(const DirDev& y, int emaj) {
   Layout L;
-  L.hb = (y.nh + 1) & ~1;
+  // element-major: the bubble blocks and every row start on a 128-byte line
+  // (16 doubles), so that the TMA boxes (128-byte rows) and the coalesced
+  // stores cover whole 32-byte sectors -- a 16-byte offset made every
+  // 128-byte row straddle 5 sectors and forced partial-sector writes
+  L.hb = emaj ? (y.nh + 15) & ~15 : (y.nh + 1) & ~1;
   L.np = (y.n + 1) & ~1;
   L.Q = (y.p - 1 + 1) & ~1;
   L.emaj = emaj;
-  L.ld = emaj ? L.hb + y.n * L.Q : L.hb + (y.p - 1) * L.np;
+  L.ld = emaj ? (L.hb + y.n * L.Q + 15) & ~15 : L.hb + (y.p - 1) * L.np;
   if (L.ld < 2) L.ld = 2;
   return L;
 }
@@ -154,6 +160,7 @@ cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const
                            cudaStream_t st);
 /* accumulate = 1: G += load(Fleg) (the variable-coefficient operator adds
  * its Hadamard term onto hpfem_apply's output) */
+cudaError_t launch_load_tab(const DirDev& d, int* r, double* w, cudaStream_t st);
 cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st,
                           int accumulate = 0, double scale = 1.0);  // G (+)= scale * load(Fleg)
 cudaError_t launch_solve1d(const DirDev& d, const FacView& f, int nrhs, const double* F, double* U,

@@ -1045,8 +1045,71 @@ __global__ void __launch_bounds__(256) k_finalize(DirDev y, int Nx, Layout L, co
   U[(size_t)i * y.N + j] = v;
 }
 
+/* Element-major layout: per row, the bubbles are an (e, k) -> (k, e)
+ * transpose; 32 x 32 tiles through shared memory keep both the internal
+ * reads (along k) and the caller-layout writes (along e) coalesced.
+ * grid (rows, e tiles, k tiles), block 32 x 8. */
+__global__ void __launch_bounds__(256) k_finalize_t(DirDev y, Layout L, const double* __restrict__ vL,
+                                                     const double* __restrict__ vR, const double* __restrict__ X,
+                                                     double* __restrict__ U) {
+  __shared__ double t[32][33];
+  const int i = blockIdx.x, e0 = blockIdx.y * 32, k0 = blockIdx.z * 32;
+  const int q = y.p - 1, n = y.n, tx = threadIdx.x, ty = threadIdx.y;
+  const double* row = X + (size_t)i * L.ld;
+  double* u = U + (size_t)i * y.N;
+  if (blockIdx.y == 0 && blockIdx.z == 0)
+    for (int j = ty * 32 + tx; j < y.nh; j += 256) u[j] = row[j];
+#pragma unroll
+  for (int ee = ty; ee < 32; ee += 8) {
+    const int e = e0 + ee, k = k0 + tx;
+    if (e < n && k < q) t[ee][tx] = row[L.hb + (size_t)e * L.Q + k];
+  }
+  __syncthreads();
+  const int e = e0 + tx;
+  if (e >= n) return;
+  const int hL = hat_of_node(e, n, y.bc), hR = hat_of_node(e + 1, n, y.bc);
+  const double xL = hL >= 0 ? row[hL] : 0.0, xR = hR >= 0 ? row[hR] : 0.0;
+#pragma unroll
+  for (int kk = ty; kk < 32; kk += 8) {
+    const int k = k0 + kk;
+    if (k >= q) break;
+    const int b = k * n + e;
+    double v = t[tx][kk];
+    if (hL >= 0) v -= __ldg(vL + b) * xL;
+    if (hR >= 0) v -= __ldg(vR + b) * xR;
+    u[y.nh + b] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_copyin_t(DirDev y, Layout L, const double* __restrict__ G,
+                                                   double* __restrict__ Gp) {
+  __shared__ double t[32][33];
+  const int i = blockIdx.x, e0 = blockIdx.y * 32, k0 = blockIdx.z * 32;
+  const int q = y.p - 1, n = y.n, tx = threadIdx.x, ty = threadIdx.y;
+  const double* g = G + (size_t)i * y.N;
+  double* o = Gp + (size_t)i * L.ld;
+  if (blockIdx.y == 0 && blockIdx.z == 0)
+    for (int j = ty * 32 + tx; j < y.nh; j += 256) o[j] = __ldg(g + j);
+#pragma unroll
+  for (int kk = ty; kk < 32; kk += 8) {
+    const int k = k0 + kk, e = e0 + tx;
+    if (k < q && e < n) t[kk][tx] = __ldg(g + y.nh + (size_t)k * n + e);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int ee = ty; ee < 32; ee += 8) {
+    const int e = e0 + ee, k = k0 + tx;
+    if (k < q && e < n) o[L.hb + (size_t)e * L.Q + k] = t[tx][ee];
+  }
+}
+
 cudaError_t launch_finalize(const DirDev& x, const DirDev& y, const Layout& L, const double* vL, const double* vR,
                             const double* X, double* U, cudaStream_t st) {
+  if (L.emaj && y.nb > 0) {
+    dim3 grid(x.N, (y.n + 31) / 32, (y.p - 1 + 31) / 32);
+    k_finalize_t<<<grid, dim3(32, 8), 0, st>>>(y, L, vL, vR, X, U);
+    return cudaGetLastError();
+  }
   dim3 grid((y.N + 255) / 256, x.N);
   k_finalize<<<grid, 256, 0, st>>>(y, x.N, L, vL, vR, X, U);
   return cudaGetLastError();
@@ -1063,6 +1126,11 @@ __global__ void __launch_bounds__(256) k_copyin(DirDev y, int Nx, Layout L, cons
 
 cudaError_t launch_copyin(const DirDev& x, const DirDev& y, const Layout& L, const double* G, double* Gp,
                           cudaStream_t st) {
+  if (L.emaj && y.nb > 0) {
+    dim3 grid(x.N, (y.n + 31) / 32, (y.p - 1 + 31) / 32);
+    k_copyin_t<<<grid, dim3(32, 8), 0, st>>>(y, L, G, Gp);
+    return cudaGetLastError();
+  }
   dim3 grid((y.N + 255) / 256, x.N);
   k_copyin<<<grid, 256, 0, st>>>(y, x.N, L, G, Gp);
   return cudaGetLastError();
@@ -1292,15 +1360,49 @@ __device__ __forceinline__ int load_sources(const DirDev& o, int l, int* r, doub
   return 0;
 }
 
+/* the load sources of every dof of one direction, tabled once per plan (the
+ * fp64 divides of load_sources would otherwise dominate k_load2d) */
+__global__ void k_load_tab(DirDev o, int* __restrict__ r, double* __restrict__ w) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= o.N) return;
+  int rr[4];
+  double ww[4];
+  load_sources(o, l, rr, ww);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    r[4 * l + q] = rr[q];
+    w[4 * l + q] = ww[q];
+  }
+}
+
+cudaError_t launch_load_tab(const DirDev& d, int* r, double* w, cudaStream_t st) {
+  if (d.N <= 0) return cudaSuccess;
+  k_load_tab<<<(d.N + 255) / 256, 256, 0, st>>>(d, r, w);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ void load_sources_tab(const DirDev& o, int l, int* r, double* w) {
+  if (o.lw) {
+    const int4 ri = *reinterpret_cast<const int4*>(o.lr + 4 * l);
+    const double4 wi = *reinterpret_cast<const double4*>(o.lw + 4 * l);
+    r[0] = ri.x; r[1] = ri.y; r[2] = ri.z; r[3] = ri.w;
+    w[0] = wi.x; w[1] = wi.y; w[2] = wi.z; w[3] = wi.w;
+  } else {
+    load_sources(o, l, r, w);
+  }
+}
+
 __global__ void __launch_bounds__(128) k_load2d(DirDev x, DirDev y, const double* __restrict__ Fl,
                                                  double* __restrict__ G, int accumulate, double scale) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
+  // rows (k, e) and (k - 2, e) share the Legendre row (k, e): take the rows
+  // element by element so that the shared source rows are re-read from L2
+  const int i = row_of(x, blockIdx.y);
   if (j >= y.N) return;
   int rx[4], ry[4];
   double wx[4], wy[4];
-  load_sources(x, i, rx, wx);
-  load_sources(y, j, ry, wy);
+  load_sources_tab(x, i, rx, wx);
+  load_sources_tab(y, j, ry, wy);
   const size_t ldl = (size_t)(y.p + 1) * y.n;
   double acc = 0.0;
 #pragma unroll

@@ -317,6 +317,7 @@ struct hpfem_plan_s {
   double* fx = nullptr;           // J sets (x-solves)
   double* fy = nullptr;           // J+1 sets (y-solves, last = mass)
   double* d_delta = nullptr;      // [n_x | n_y]
+  double* d_ldtab = nullptr;      // load-source tables of both directions (DirDev::lw / lr)
   double* d_shift = nullptr;      // kap/sig arrays
   double* d_tau = nullptr;        // apply shifts [hw2 - p_j | hw2 + q_j] (K11)
   int* d_err = nullptr;
@@ -397,6 +398,7 @@ void free_plan(hpfem_plan_t pl) {
   cudaFree(pl->fx);
   cudaFree(pl->fy);
   cudaFree(pl->d_delta);
+  cudaFree(pl->d_ldtab);
   cudaFree(pl->d_shift);
   cudaFree(pl->d_tau);
   cudaFree(pl->d_err);
@@ -522,10 +524,25 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
     DirDev d;
     d.n = h.n; d.p = h.p; d.bc = h.bc; d.nh = h.nh; d.N = h.N; d.nb = h.nb; d.delta = dd;
     d.rob0 = h.rob[0]; d.rob1 = h.rob[1];
+    d.lw = nullptr; d.lr = nullptr;
     return d;
   };
   pl->dx = mkdev(hx, pl->d_delta);
   pl->dy = mkdev(hy, pl->d_delta + nx);
+  {  // load-source tables ([N][4] weights, then [N][4] rows) of both directions
+    const size_t nxy = (size_t)pl->dx.N + pl->dy.N;
+    if ((ce = cudaMalloc(&pl->d_ldtab, nxy * 4 * (sizeof(double) + sizeof(int)))) != cudaSuccess)
+      return fail_cuda(ce, "alloc");
+    double* w = pl->d_ldtab;
+    int* r = reinterpret_cast<int*>(w + 4 * nxy);
+    pl->dx.lw = w;
+    pl->dx.lr = r;
+    pl->dy.lw = w + 4 * (size_t)pl->dx.N;
+    pl->dy.lr = r + 4 * (size_t)pl->dx.N;
+    if ((ce = launch_load_tab(pl->dx, const_cast<int*>(pl->dx.lr), const_cast<double*>(pl->dx.lw), st)) != cudaSuccess ||
+        (ce = launch_load_tab(pl->dy, const_cast<int*>(pl->dy.lr), const_cast<double*>(pl->dy.lw), st)) != cudaSuccess)
+      return fail_cuda(ce, "load tables");
+  }
   pl->sx = fac_stride(pl->dx);
   pl->sy = fac_stride(pl->dy);
   // shift parameter tables: x: J sets (kap=1, sig = w^2/2 - q_j); y: J sets (sig = w^2/2 + p_j) + mass
