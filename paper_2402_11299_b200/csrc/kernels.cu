@@ -1392,12 +1392,21 @@ __device__ __forceinline__ void load_sources_tab(const DirDev& o, int l, int* r,
   }
 }
 
+/* y-direction part of one source row: t = sum_b wy_b F(row, ry_b) */
+__device__ __forceinline__ double load_trow(const double* __restrict__ Fl, size_t ldl, int row, const int* ry,
+                                            const double* wy) {
+  double t = 0.0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (ry[b] >= 0) t += wy[b] * __ldg(Fl + (size_t)row * ldl + ry[b]);
+  return t;
+}
+
+/* generic rows (the x-hat rows here): G(i, j) = sum_a wx_a t(rx_a) */
 __global__ void __launch_bounds__(128) k_load2d(DirDev x, DirDev y, const double* __restrict__ Fl,
-                                                 double* __restrict__ G, int accumulate, double scale) {
+                                                 double* __restrict__ G, int accumulate, double scale, int row0) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  // rows (k, e) and (k - 2, e) share the Legendre row (k, e): take the rows
-  // element by element so that the shared source rows are re-read from L2
-  const int i = row_of(x, blockIdx.y);
+  const int i = row_of(x, row0 + blockIdx.y);
   if (j >= y.N) return;
   int rx[4], ry[4];
   double wx[4], wy[4];
@@ -1408,15 +1417,46 @@ __global__ void __launch_bounds__(128) k_load2d(DirDev x, DirDev y, const double
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     if (rx[a] < 0) continue;
-    double t = 0.0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-      if (ry[b] >= 0) t += wy[b] * __ldg(Fl + (size_t)rx[a] * ldl + ry[b]);
-    acc += wx[a] * t;
+    acc += wx[a] * load_trow(Fl, ldl, rx[a], ry, wy);
   }
   acc *= scale;
   if (accumulate) acc += G[(size_t)i * y.N + j];
   G[(size_t)i * y.N + j] = acc;
+}
+
+/* x-bubble rows (k, e_x), k in [k0, k0 + KB): their sources are the Legendre
+ * rows (k, e_x) and (k + 2, e_x) (load_sources), so each y-contracted source
+ * row t(m) is formed once and used by the outputs k = m and k = m - 2 (same
+ * expressions as k_load2d, i.e. bitwise the same G).  grid (column blocks,
+ * x-elements, degree chunks). */
+constexpr int LOAD_KB = 16;
+__global__ void __launch_bounds__(128) k_load2d_bub(DirDev x, DirDev y, const double* __restrict__ Fl,
+                                                     double* __restrict__ G, int accumulate, double scale) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ex = blockIdx.y, k0 = blockIdx.z * LOAD_KB, n = x.n, q = x.p - 1;
+  if (j >= y.N) return;
+  int ry[4];
+  double wy[4];
+  load_sources_tab(y, j, ry, wy);
+  const size_t ldl = (size_t)(y.p + 1) * y.n;
+  const int k1 = k0 + LOAD_KB < q ? k0 + LOAD_KB : q;
+  double t0 = load_trow(Fl, ldl, k0 * n + ex, ry, wy);
+  double t1 = k0 + 1 < k1 ? load_trow(Fl, ldl, (k0 + 1) * n + ex, ry, wy) : 0.0;
+  for (int k = k0; k < k1; ++k) {
+    const int i = x.nh + k * n + ex;
+    int rx[4];
+    double wx[4];
+    load_sources_tab(x, i, rx, wx);  // rx = {(k, ex), (k + 2, ex), -1, -1}
+    const double t2 = load_trow(Fl, ldl, rx[1], ry, wy);
+    double acc = 0.0;
+    acc += wx[0] * t0;
+    acc += wx[1] * t2;
+    acc *= scale;
+    if (accumulate) acc += G[(size_t)i * y.N + j];
+    G[(size_t)i * y.N + j] = acc;
+    t0 = t1;
+    t1 = t2;
+  }
 }
 
 /* Unload (NEXT-1): Legendre coefficient (degree m, element e) of direction
@@ -1504,8 +1544,17 @@ cudaError_t launch_unload2d(const DirDev& x, const DirDev& y, const double* U, d
 
 cudaError_t launch_load2d(const DirDev& x, const DirDev& y, const double* Fleg, double* G, cudaStream_t st,
                           int accumulate, double scale) {
+  if (x.lw && x.nb > 0) {  // bubble rows by element and degree chunk, then the hat rows
+    dim3 gb((y.N + 127) / 128, x.n, (x.p - 1 + LOAD_KB - 1) / LOAD_KB);
+    k_load2d_bub<<<gb, 128, 0, st>>>(x, y, Fleg, G, accumulate, scale);
+    if (x.nh > 0) {
+      dim3 gh((y.N + 127) / 128, x.nh);
+      k_load2d<<<gh, 128, 0, st>>>(x, y, Fleg, G, accumulate, scale, x.nb);
+    }
+    return cudaGetLastError();
+  }
   dim3 grid((y.N + 127) / 128, x.N);
-  k_load2d<<<grid, 128, 0, st>>>(x, y, Fleg, G, accumulate, scale);
+  k_load2d<<<grid, 128, 0, st>>>(x, y, Fleg, G, accumulate, scale, 0);
   return cudaGetLastError();
 }
 
