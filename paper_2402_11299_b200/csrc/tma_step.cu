@@ -452,6 +452,15 @@ __global__ void __launch_bounds__(NT, 1)
     const int rh1 = EG + eo;            //   hR
     double ys[CL];
     double yv = 0.0;
+    // Software-pipelined down sweep: the stencil of stage sg (independent
+    // shared-memory loads and FMAs) is interleaved position by position with
+    // the dependent recurrence of the previous stage sg + 1, so each warp has
+    // independent work to issue under the FMA latency of its chain.  The
+    // arithmetic per position is unchanged (bitwise the same result).
+    // Positions past this parity's chain have zero factors (fac_cfs) and
+    // finite (zero-padded) inputs: yv stays exactly 0 there, no select on the
+    // dependent chain.
+    double rv[KCP];
 #pragma unroll
     for (int sg = CL / KCP - 1; sg >= 0; --sg) {
       if (KCP * sg < my) {
@@ -472,14 +481,20 @@ __global__ void __launch_bounds__(NT, 1)
         const double* Gs = reinterpret_cast<const double*>(stg);
         const double* Ws = reinterpret_cast<const double*>(stg + A.off_w);
         const double* Hs = reinterpret_cast<const double*>(stg + A.off_h);
-        double rv[KCP];
+        const bool prev = sg + 1 < CL / KCP && KCP * (sg + 1) < my;  // stage sg + 1 awaits its recurrence
 #pragma unroll
-        for (int u = 0; u < KCP; ++u) {
+        for (int u = KCP - 1; u >= 0; --u) {
           double v = 0.0;
           if (MODE != ST_CORR) v = Gs[swz(rg, u, py)];
           if (MODE != ST_NONE)
             v += st.w[0] * Ws[swz(rw0, u, py)] + st.w[1] * Ws[swz(rw1, u, py)] + st.w[2] * Ws[swz(rw2, u, py)] +
                  st.w[3] * Hs[swz(rh0, u, py)] + st.w[4] * Hs[swz(rh1, u, py)];
+          if (sg + 1 < CL / KCP && prev) {
+            const int c = KCP * (sg + 1) + u;
+            const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c);  // (il, hd)
+            yv = fma(-f.y, yv, f.x * rv[u]);
+            ys[c] = yv;
+          }
           rv[u] = v;
         }
         __syncwarp();
@@ -490,17 +505,13 @@ __global__ void __launch_bounds__(NT, 1)
           cslot = 0;
           ++cround;
         }
-#pragma unroll
-        for (int u = KCP - 1; u >= 0; --u) {
-          const int c = KCP * sg + u;
-          // positions past this parity's chain have zero factors (fac_cfs) and
-          // finite (zero-padded) inputs: yv stays exactly 0 there, no select
-          // on the dependent chain
-          const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c);  // (il, hd)
-          yv = fma(-f.y, yv, f.x * rv[u]);
-          ys[c] = yv;
-        }
       }
+    }
+#pragma unroll
+    for (int u = KCP - 1; u >= 0; --u) {  // the recurrence of stage 0
+      const double2 f = *reinterpret_cast<const double2*>(fb + 4 * u);
+      yv = fma(-f.y, yv, f.x * rv[u]);
+      ys[u] = yv;
     }
     // upward sweep, staged per warp through shared memory and stored with TMA
     // per 16 degrees (one box of this warp's RW rows; no CTA-wide barrier)
