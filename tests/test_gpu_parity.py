@@ -83,6 +83,33 @@ def test_small_cases(case, kernel_path):
     assert l2 <= L2_TOL
 
 
+MANY_HATS = [
+    # one direction with ~1000 hats: the hat Schur kernel's [hats][32 lines]
+    # tile exceeds shared memory and it falls back to 8 lines per CTA
+    (rmesh(1000, 0, 1, 21), 2, rmesh(3, 0, 1, 22), 18, 1.0, 0, 1e-10),
+    (rmesh(3, 0, 2, 23), 18, rmesh(1000, 0, 1, 24), 2, 0.5, 1, 1e-10),
+]
+
+
+@pytest.mark.parametrize("case", range(len(MANY_HATS)))
+def test_many_hats(case):
+    """Solve and load with ~1000 hats in one direction vs the oracle."""
+    xs, px, ys, py, om, bc, tol = MANY_HATS[case]
+    plan = gpu_plan(xs, px, ys, py, om, bc, tol)
+    ref = oracle.plan(xs, px, ys, py, om, bc, tol)
+    assert plan.J == ref["J"]
+    G = RNG.standard_normal((plan.Nx, plan.Ny))
+    U = gpu_solve(plan, G)
+    Uref, J = oracle.adi_solve(xs, px, ys, py, om, bc, tol, G)
+    l2, plain = parity(xs, px, ys, py, bc, U, Uref)
+    print(f"many hats {case}: N={plan.Nx}x{plan.Ny} J={J} L2 {l2:.2e} plain {plain:.2e}")
+    assert l2 <= L2_TOL
+    Fleg = RNG.standard_normal(((px + 1) * (len(xs) - 1), (py + 1) * (len(ys) - 1)))
+    Gl = gpu_load(plan, Fleg)
+    Gref = oracle.load(xs, px, ys, py, bc, Fleg)
+    assert np.abs(Gl - Gref).max() <= 1e-14 * np.abs(Gref).max()
+
+
 @pytest.mark.parametrize("case", [3, 4, 5, 7, 12, 13, 14])
 def test_lemma51_against_dense(case):
     """The GPU solution itself meets Lemma 5.1 against the dense
