@@ -534,6 +534,19 @@ __global__ void __launch_bounds__(NT, 1)
         t_br += clock64() - t0;
 #endif
 #pragma unroll
+        // the group's factor pairs first: in program order after the staging
+        // stores they could not be hoisted (the compiler cannot rule out
+        // aliasing in shared memory) and each step waited a load latency
+        double2 fz[SPB][KCP];
+#pragma unroll
+        for (int h = 0; h < SPB; ++h) {
+          const int sg = sp + h;
+          if (sg < CL / KCP && KCP * sg < my) {
+#pragma unroll
+            for (int u = 0; u < KCP; ++u) fz[h][u] = *reinterpret_cast<const double2*>(fb + 4 * (KCP * sg + u) + 2);
+          }
+        }
+#pragma unroll
         for (int h = 0; h < SPB; ++h) {
           const int sg = sp + h;
           if (sg < CL / KCP && KCP * sg < my) {
@@ -541,7 +554,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int u = 0; u < KCP; ++u) {
               const int c = KCP * sg + u;
-              const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c + 2);  // (hu, il)
+              const double2 f = fz[h][u];  // (hu, il)
               z = fma(-f.x, z, f.y * ys[c]);  // 0 past the chain (see above)
               o[swz((r - wr0) * EG + eo, u, py)] = valid ? z : 0.0;
               if (sg == 0 && u == 0 && valid && c < mthr && P.z01)  // chain-first bubble (degree py): compact copy
