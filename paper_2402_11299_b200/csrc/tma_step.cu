@@ -316,12 +316,21 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
     if (valid) {
       double* __restrict__ out = P.out + P.lay.hb + (size_t)ey * Q + ky;
       double z = 0.0;
+      // factor pairs loaded KR at a time ahead of the stores (as in the y-solve)
 #pragma unroll
-      for (int c = 0; c < CL; ++c) {
-        if (c < m) {
-          const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c + 2);  // (hu, il)
-          z = fma(-f.x, z, f.y * ys[c]);
-          out[(size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld] = z;
+      for (int c0 = 0; c0 < CL; c0 += KR) {
+        if (c0 < m) {
+          double2 fz[KR];
+#pragma unroll
+          for (int u = 0; u < KR; ++u) fz[u] = *reinterpret_cast<const double2*>(fb + 4 * (c0 + u) + 2);  // (hu, il)
+#pragma unroll
+          for (int u = 0; u < KR; ++u) {
+            const int c = c0 + u;
+            if (c < m) {
+              z = fma(-fz[u].x, z, fz[u].y * ys[c]);
+              out[(size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld] = z;
+            }
+          }
         }
       }
     }
