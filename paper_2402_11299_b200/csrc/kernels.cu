@@ -743,7 +743,10 @@ static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
 /* y-solve, lines = x-hat rows t: CTA = (t, group of EGH y-elements).
  * smem: 8 row segments [EGH*Q] (G + 7 stencil rows) and the chains'
  * factors [EGH][2][cfs]. */
-constexpr int EGH = 8;
+#ifndef HPFEM_EGH
+#define HPFEM_EGH 4
+#endif
+constexpr int EGH = HPFEM_EGH;  // y-elements per hat-row CTA
 
 /* In-place solve of one bubble chain held in shared memory, v[c * vs],
  * c < m, with the chain-major factors f ([4c] il, [4c+1] g il, [4c+2]
