@@ -688,7 +688,16 @@ static cudaError_t launch_bub_dir(const StepParams& P, cudaStream_t st) {
     if (m <= 32) return launch_bub_reg<DIR, 32>(P, st);
     return launch_bub_reg<DIR, 64>(P, st);
   }
-  constexpr int U = 8;
+#ifndef HPFEM_LDG_UX
+#define HPFEM_LDG_UX 4
+#endif
+#ifndef HPFEM_LDG_UY
+#define HPFEM_LDG_UY 2
+#endif
+  // chain positions per load batch: smaller batches (fewer registers, more
+  // resident threads) measured faster, most for the long y chains of
+  // config 4 (p = 256: U 8 -> 2 cut the y kernel 1.48 -> 1.07 ms; x: U 4)
+  constexpr int U = DIR == 0 ? HPFEM_LDG_UX : HPFEM_LDG_UY;
   if (DIR == 0) {
     dim3 grid((P.lp_count + 255) / 256, P.s.n * 2);
     k_bubbles<DIR, U><<<grid, 256, 0, st>>>(P);
