@@ -106,6 +106,13 @@ int hpfem_plan_robin(const double* xs, int n_x, int p_x, const double* ys, int n
 int hpfem_plan_info(hpfem_plan_t plan, int* N_x, int* N_y, int* J, double* lam_x /*[2]*/, double* lam_y /*[2]*/,
                     double* gamma);
 
+/* Mesh sizes of the plan (host outputs; any pointer may be NULL): elements
+ * and degree per direction.  The Legendre-coefficient arrays of hpfem_load /
+ * hpfem_unload / hpfem_transform are ((p_x+1) n_x) x ((p_y+1) n_y); the
+ * bindings use this to check array sizes before a call (the C ABI takes raw
+ * pointers and cannot). */
+int hpfem_plan_dims(hpfem_plan_t plan, int* n_x, int* p_x, int* n_y, int* p_y);
+
 /* Host copies of the shifts: p[0..J-1] (used by the y-solves and the
  * x-applies), q[0..J-1] (x-solves and y-applies), ascending j. */
 int hpfem_plan_shifts(hpfem_plan_t plan, double* p, double* q);

@@ -271,3 +271,39 @@ def l2_rel_diff(xs, px, ys, py, bc, U, Uref):
     d = l2_norm_sq(xs, px, ys, py, bc, np.asarray(U) - np.asarray(Uref))
     r = l2_norm_sq(xs, px, ys, py, bc, Uref)
     return float(np.sqrt(max(d, 0.0) / r))
+
+
+def rel_diffs(xs, px, ys, py, bc, U, Uref):
+    """(L2(Omega) relative, plain coefficient 2-norm relative, max-abs
+    relative) differences of two coefficient arrays: the three parity
+    measures (reading R12; the last two weight every coefficient alike)."""
+    U, Uref = np.asarray(U), np.asarray(Uref)
+    d = U - Uref
+    nr = np.linalg.norm(Uref)
+    mr = np.abs(Uref).max() if Uref.size else 0.0
+    return (l2_rel_diff(xs, px, ys, py, bc, U, Uref) if nr > 0 else float(np.linalg.norm(d)),
+            float(np.linalg.norm(d) / nr) if nr > 0 else float(np.linalg.norm(d)),
+            float(np.abs(d).max() / mr) if mr > 0 else float(np.abs(d).max(initial=0.0)))
+
+
+def rounding_floor(xs, px, ys, py, omega, bc, tol, G, iters=-1):
+    """The oracle's own fp64 reproducibility floor for one problem: the
+    rel_diffs between adi_solve(G) and adi_solve of the same problem
+    perturbed at the rounding level -- G * (1 + 1e-16 N(0,1)) (seed 5), and
+    every interior breakpoint scaled by 1 + 2^-52.  Two correct fp64
+    implementations of Algorithm 2 that round differently cannot be expected
+    to agree better than this.  Returns a dict with the
+    *_l2 / *_plain / *_max floors of both perturbations."""
+    U1, J = adi_solve(xs, px, ys, py, omega, bc, tol, G, iters)
+    rng = np.random.default_rng(5)
+    G = _f64(G)
+    U2, _ = adi_solve(xs, px, ys, py, omega, bc, tol, G * (1 + 1e-16 * rng.standard_normal(G.shape)), iters)
+    g = rel_diffs(xs, px, ys, py, bc, U2, U1)
+    del U2
+    xs2, ys2 = np.array(xs, dtype=np.float64), np.array(ys, dtype=np.float64)
+    xs2[1:-1] *= 1 + 2.0 ** -52
+    ys2[1:-1] *= 1 + 2.0 ** -52
+    U3, _ = adi_solve(xs2, px, ys2, py, omega, bc, tol, G, iters)
+    m = rel_diffs(xs, px, ys, py, bc, U3, U1)
+    return dict(J=J, iters=iters, G_perturb_l2=g[0], G_perturb_plain=g[1], G_perturb_max=g[2], mesh_ulp_l2=m[0],
+                mesh_ulp_plain=m[1], mesh_ulp_max=m[2]), U1

@@ -54,6 +54,7 @@ def _load():
     L.hpfem_plan_robin.argtypes = [_dp, _i, _i, _dp, _i, _i, _d, _i, _dp, _d, _vp, ctypes.POINTER(_vp)]
     L.hpfem_plan_info.argtypes = [_vp, _ip, _ip, _ip, _dp, _dp, _dp]
     L.hpfem_plan_shifts.argtypes = [_vp, _dp, _dp]
+    L.hpfem_plan_dims.argtypes = [_vp, _ip, _ip, _ip, _ip]
     L.hpfem_solve.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_solve_iters.argtypes = [_vp, _vp, _vp, _i, _vp]
     L.hpfem_apply.argtypes = [_vp, _vp, _vp, _vp]
@@ -76,7 +77,7 @@ def _load():
     L.hpfem_plan_destroy.argtypes = [_vp]
     L.hpfem_plan_destroy.restype = None
     L.hpfem_last_error.restype = ctypes.c_char_p
-    for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
+    for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_dims", "hpfem_plan_shifts", "hpfem_solve",
               "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
               "hpfem_plan_profile_read", "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_grid",
               "hpfem_transform", "hpfem_itransform", "hpfem_varcoef_apply", "hpfem_pcg", "hpfem_imex_step"):
@@ -85,7 +86,7 @@ def _load():
     return L
 
 
-EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_shifts", "hpfem_solve",
+EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_dims", "hpfem_plan_shifts", "hpfem_solve",
            "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
            "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error",
            "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_plan1d_destroy",
@@ -120,6 +121,15 @@ def _ptr(x) -> int:
     if x.dtype != torch.float64:
         raise ValueError("expected float64")
     return x.data_ptr()
+
+
+def _sized(x, n: int, what: str) -> int:
+    """_ptr(x) after checking that the tensor holds exactly n doubles: the C
+    ABI takes raw pointers and cannot check sizes, so an undersized buffer
+    would be read / written past its end.  Raw ints are passed unchecked."""
+    if not isinstance(x, int) and x.numel() != n:
+        raise ValueError(f"{what}: expected {n} float64 elements, got {x.numel()} (shape {tuple(x.shape)})")
+    return _ptr(x)
 
 
 def _stream(stream) -> int:
@@ -166,6 +176,24 @@ def hpfem_plan_info(plan: int) -> dict:
     return dict(Nx=Nx.value, Ny=Ny.value, J=J.value, lam_x=np.array(lx[:]), lam_y=np.array(ly[:]), gamma=g.value)
 
 
+def hpfem_plan_dims(plan: int) -> dict:
+    nx, px, ny, py = _i(), _i(), _i(), _i()
+    _check(_load().hpfem_plan_dims(plan, ctypes.byref(nx), ctypes.byref(px), ctypes.byref(ny), ctypes.byref(py)))
+    return dict(nx=nx.value, px=px.value, ny=ny.value, py=py.value)
+
+
+def _nn(plan: int) -> int:
+    """N_x N_y: elements of a solution / load-space array."""
+    i = hpfem_plan_info(plan)
+    return i["Nx"] * i["Ny"]
+
+
+def _nleg(plan: int) -> int:
+    """((p_x+1) n_x) ((p_y+1) n_y): elements of a Legendre / grid array."""
+    d = hpfem_plan_dims(plan)
+    return (d["px"] + 1) * d["nx"] * (d["py"] + 1) * d["ny"]
+
+
 def hpfem_plan_shifts(plan: int):
     J = hpfem_plan_info(plan)["J"]
     p, q = np.empty(J), np.empty(J)
@@ -174,15 +202,18 @@ def hpfem_plan_shifts(plan: int):
 
 
 def hpfem_solve(plan: int, F, U, stream=None):
-    _check(_load().hpfem_solve(plan, _ptr(F), _ptr(U), _stream(stream)))
+    n = _nn(plan)
+    _check(_load().hpfem_solve(plan, _sized(F, n, "F"), _sized(U, n, "U"), _stream(stream)))
 
 
 def hpfem_solve_iters(plan: int, F, U, iters: int, stream=None):
-    _check(_load().hpfem_solve_iters(plan, _ptr(F), _ptr(U), iters, _stream(stream)))
+    n = _nn(plan)
+    _check(_load().hpfem_solve_iters(plan, _sized(F, n, "F"), _sized(U, n, "U"), iters, _stream(stream)))
 
 
 def hpfem_solve_batched(plan: int, batch: int, F, U, stream=None):
-    _check(_load().hpfem_solve_batched(plan, batch, _ptr(F), _ptr(U), _stream(stream)))
+    n = _nn(plan) * max(batch, 0)
+    _check(_load().hpfem_solve_batched(plan, batch, _sized(F, n, "F"), _sized(U, n, "U"), _stream(stream)))
 
 
 def hpfem_plan1d(xs, p: int, bc: int, omega: float, stream=None) -> int:
@@ -199,7 +230,8 @@ def hpfem_plan1d_info(plan: int) -> int:
 
 
 def hpfem_solve1d(plan: int, nrhs: int, F, U, stream=None):
-    _check(_load().hpfem_solve1d(plan, nrhs, _ptr(F), _ptr(U), _stream(stream)))
+    n = hpfem_plan1d_info(plan) * max(nrhs, 0)
+    _check(_load().hpfem_solve1d(plan, nrhs, _sized(F, n, "F"), _sized(U, n, "U"), _stream(stream)))
 
 
 def hpfem_plan1d_destroy(plan: int):
@@ -232,15 +264,16 @@ class Plan1D:
 
 
 def hpfem_apply(plan: int, U, F, stream=None):
-    _check(_load().hpfem_apply(plan, _ptr(U), _ptr(F), _stream(stream)))
+    n = _nn(plan)
+    _check(_load().hpfem_apply(plan, _sized(U, n, "U"), _sized(F, n, "F"), _stream(stream)))
 
 
 def hpfem_load(plan: int, F_leg, G, stream=None):
-    _check(_load().hpfem_load(plan, _ptr(F_leg), _ptr(G), _stream(stream)))
+    _check(_load().hpfem_load(plan, _sized(F_leg, _nleg(plan), "F_leg"), _sized(G, _nn(plan), "G"), _stream(stream)))
 
 
 def hpfem_unload(plan: int, U, C_leg, stream=None):
-    _check(_load().hpfem_unload(plan, _ptr(U), _ptr(C_leg), _stream(stream)))
+    _check(_load().hpfem_unload(plan, _sized(U, _nn(plan), "U"), _sized(C_leg, _nleg(plan), "C_leg"), _stream(stream)))
 
 
 def hpfem_grid(plan: int, Lx: int, Ly: int):
@@ -251,27 +284,33 @@ def hpfem_grid(plan: int, Lx: int, Ly: int):
 
 
 def hpfem_transform(plan: int, V, C, stream=None):
-    _check(_load().hpfem_transform(plan, _ptr(V), _ptr(C), _stream(stream)))
+    n = _nleg(plan)
+    _check(_load().hpfem_transform(plan, _sized(V, n, "V"), _sized(C, n, "C"), _stream(stream)))
 
 
 def hpfem_itransform(plan: int, C, V, stream=None):
-    _check(_load().hpfem_itransform(plan, _ptr(C), _ptr(V), _stream(stream)))
+    n = _nleg(plan)
+    _check(_load().hpfem_itransform(plan, _sized(C, n, "C"), _sized(V, n, "V"), _stream(stream)))
 
 
 def hpfem_varcoef_apply(plan: int, cgrid, U, F, stream=None):
-    _check(_load().hpfem_varcoef_apply(plan, _ptr(cgrid), _ptr(U), _ptr(F), _stream(stream)))
+    n = _nn(plan)
+    _check(_load().hpfem_varcoef_apply(plan, _sized(cgrid, _nleg(plan), "cgrid"), _sized(U, n, "U"), _sized(F, n, "F"),
+                                       _stream(stream)))
 
 
 def hpfem_pcg(plan: int, cgrid, G, U, rtol: float, maxit: int, stream=None):
     """Returns (iterations, relative residual)."""
     it, rel = _i(0), _d(0.0)
-    _check(_load().hpfem_pcg(plan, _ptr(cgrid), _ptr(G), _ptr(U), rtol, maxit, ctypes.byref(it), ctypes.byref(rel),
-                             _stream(stream)))
+    n = _nn(plan)
+    _check(_load().hpfem_pcg(plan, _sized(cgrid, _nleg(plan), "cgrid"), _sized(G, n, "G"), _sized(U, n, "U"), rtol, maxit,
+                             ctypes.byref(it), ctypes.byref(rel), _stream(stream)))
     return it.value, rel.value
 
 
 def hpfem_imex_step(plan: int, dt: float, U_leg, U_next, stream=None):
-    _check(_load().hpfem_imex_step(plan, dt, _ptr(U_leg), _ptr(U_next), _stream(stream)))
+    n = _nleg(plan)
+    _check(_load().hpfem_imex_step(plan, dt, _sized(U_leg, n, "U_leg"), _sized(U_next, n, "U_next"), _stream(stream)))
 
 
 def hpfem_plan_launches(plan: int) -> int:

@@ -113,6 +113,31 @@ inline Layout make_layout(const DirDev& y, int emaj) {
   return L;
 }
 
+/* Tuning switches, read from the environment ONCE per plan (read_tuning in
+ * plan.cpp) and carried with every launch -- no process-wide statics, so
+ * plans on several host threads / devices do not race (defaults in
+ * parentheses; all are experiment knobs). */
+struct Tuning {
+  int hat_sms;        // HPFEM_HAT_SMS (4): SMs the persistent TMA grid leaves to the side-stream hat lines
+  int no_graph;       // HPFEM_NO_GRAPH (0)
+  int no_small;       // HPFEM_NO_SMALL (0)
+  int no_tma;         // HPFEM_NO_TMA (0)
+  int no_wtab;        // HPFEM_NO_WTAB (0)
+  int batch_streams;  // HPFEM_BATCH_STREAMS (8)
+  int bub_reg;        // HPFEM_BUBBLE_KERNEL=reg (0): register variant of the LDG bubble kernel
+  int hat_lb[2];      // HPFEM_HAT_LB_X / _Y (32): lines per hat Schur CTA
+  int nst[2];         // HPFEM_NST_X / _Y (4): TMA ring depth
+  int eg_y;           // HPFEM_EG_Y (0 = automatic): y-solve tile width
+  int fake_stencil;   // HPFEM_FAKE_STENCIL (0): experiment only
+  int persist;        // HPFEM_PERSIST (1): persistent one-launch solve for L2-resident problems
+};
+
+/* Raise a kernel's dynamic shared-memory limit to `bytes` on the CURRENT
+ * device, once per (kernel, device) (kernels.cu; mutex-protected, so host
+ * threads may share the library).  cudaFuncSetAttribute can serialise with
+ * in-flight launches of the same kernel, hence the cache. */
+cudaError_t smem_optin(const void* func, size_t bytes);
+
 /* cross-line stencil mode of a half-step kernel */
 enum StencilMode { ST_NONE = 0, ST_APPLY = 1, ST_CORR = 2 };
 
@@ -144,6 +169,7 @@ struct StepParams {
    * right-hand side touch -- contiguous instead of 16 bytes out of every Q. */
   double* z01;         // y-solves: written for every row of out
   const double* z01p;  // x-solves: the copy belonging to Xp
+  Tuning tun;          // host-side launch choices (not read by the kernels)
 };
 
 /* launchers (kernels.cu); return cudaError_t of the launch */

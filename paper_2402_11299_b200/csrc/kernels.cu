@@ -23,12 +23,30 @@
  */
 #include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "hpfem_internal.h"
 #include "ops1d.h"
 #include "ptx.cuh"
 
 namespace hpfem {
+
+cudaError_t smem_optin(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;  // (kernel, device) -> opted-in bytes
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{func, dev}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 /* ------------------------------------------------------------------ */
 /* K1: factorisation of a batch of shifted 1D operators               */
@@ -657,15 +675,6 @@ __global__ void __launch_bounds__(256, 4) k_hats(StepParams P) {
   }
 }
 
-static int bubble_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HPFEM_BUBBLE_KERNEL");
-    v = (e && e[0] == 'r') ? 1 : 0;  // "reg" selects the register variant
-  }
-  return v;
-}
-
 template <int DIR, int CL>
 static cudaError_t launch_bub_reg(const StepParams& P, cudaStream_t st) {
   if (DIR == 0) {
@@ -681,7 +690,7 @@ static cudaError_t launch_bub_reg(const StepParams& P, cudaStream_t st) {
 template <int DIR>
 static cudaError_t launch_bub_dir(const StepParams& P, cudaStream_t st) {
   const int m = chain_len(P.s.p, 0);
-  if (bubble_variant() == 1 && m <= 64) {
+  if (P.tun.bub_reg && m <= 64) {  // HPFEM_BUBBLE_KERNEL=reg
     if (m <= 4) return launch_bub_reg<DIR, 4>(P, st);
     if (m <= 8) return launch_bub_reg<DIR, 8>(P, st);
     if (m <= 16) return launch_bub_reg<DIR, 16>(P, st);
@@ -716,12 +725,8 @@ cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st) {
 template <int DIR, int LB>
 static cudaError_t launch_hats_lb(const StepParams& P, cudaStream_t st) {
   const size_t smem = sizeof(double) * hats_smem_doubles(P.s.nh, LB);
-  static size_t opted = 48 * 1024;
-  if (smem > opted) {
-    cudaError_t e = cudaFuncSetAttribute(k_hats<DIR, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    opted = smem;
-  }
+  cudaError_t e = smem_optin((const void*)k_hats<DIR, LB>, smem);
+  if (e != cudaSuccess) return e;
   const int nlines = DIR == 0 ? P.ld : P.o.N;  // x-solve: internal columns (padding skipped)
   k_hats<DIR, LB><<<(nlines + LB - 1) / LB, 256, smem, st>>>(P);
   return cudaGetLastError();
@@ -731,11 +736,7 @@ static cudaError_t launch_hats_lb(const StepParams& P, cudaStream_t st) {
  * fewer when the [nh][LB] tile would not fit in shared memory (many hats) */
 template <int DIR>
 static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
-  static int lb = -1;
-  if (lb < 0) {
-    const char* v = getenv(DIR == 0 ? "HPFEM_HAT_LB_X" : "HPFEM_HAT_LB_Y");
-    lb = v && *v ? atoi(v) : 32;
-  }
+  const int lb = P.tun.hat_lb[DIR];
   const size_t cap = 227 * 1024;
   if (lb != 8 && sizeof(double) * hats_smem_doubles(P.s.nh, 32) <= cap) return launch_hats_lb<DIR, 32>(P, st);
   if (sizeof(double) * hats_smem_doubles(P.s.nh, 8) <= cap) return launch_hats_lb<DIR, 8>(P, st);
@@ -1006,23 +1007,15 @@ cudaError_t launch_hat_lines(const StepParams& P, cudaStream_t st) {
   const Layout& L = P.lay;
   if (P.dir == 1) {
     const size_t smem = sizeof(double) * (8 * (size_t)EGH * L.Q + (size_t)EGH * 2 * P.f.cfs);
-    static size_t opted = 48 * 1024;
-    if (smem > opted) {
-      cudaError_t e = cudaFuncSetAttribute(k_hatrows_y, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      opted = smem;
-    }
+    cudaError_t e = smem_optin((const void*)k_hatrows_y, smem);
+    if (e != cudaSuccess) return e;
     dim3 grid(P.o.nh, (P.s.n + EGH - 1) / EGH);
     k_hatrows_y<<<grid, 128, smem, st>>>(P);
   } else {
     const int m = chain_len(P.s.p, 0);
     const size_t smem = sizeof(double) * ((size_t)m * (TC + HREG + 2 * (TC + 2)) + P.f.cfs);
-    static size_t opted = 48 * 1024;
-    if (smem > opted) {
-      cudaError_t e = cudaFuncSetAttribute(k_hatcols_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      opted = smem;
-    }
+    cudaError_t e = smem_optin((const void*)k_hatcols_x, smem);
+    if (e != cudaSuccess) return e;
     dim3 grid(P.s.n * 2, (P.o.nh + TC - 1) / TC);
     k_hatcols_x<<<grid, 256, smem, st>>>(P);
   }
@@ -1331,12 +1324,8 @@ size_t small_smem_bytes(const DirDev& x, const DirDev& y) {
 
 cudaError_t launch_adi_small(const SmallArgs& a, int batch, cudaStream_t st) {
   const size_t smem = small_smem_bytes(a.x, a.y);
-  static size_t opted = 48 * 1024;
-  if (smem > opted) {
-    cudaError_t e = cudaFuncSetAttribute(k_adi_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    opted = smem;
-  }
+  cudaError_t e = smem_optin((const void*)k_adi_small, smem);
+  if (e != cudaSuccess) return e;
   k_adi_small<<<batch, 256, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -41,6 +41,33 @@ int cuda_err(cudaError_t e, const char* where) {
   return set_err(HPFEM_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+/* the tuning switches (hpfem_internal.h Tuning), read once per plan */
+Tuning read_tuning() {
+  Tuning t;
+  t.hat_sms = env_int("HPFEM_HAT_SMS", 4);
+  t.no_graph = env_int("HPFEM_NO_GRAPH", 0) == 1;
+  t.no_small = env_int("HPFEM_NO_SMALL", 0) == 1;
+  t.no_tma = env_int("HPFEM_NO_TMA", 0) == 1;
+  t.no_wtab = env_int("HPFEM_NO_WTAB", 0) == 1;
+  t.batch_streams = env_int("HPFEM_BATCH_STREAMS", 8);
+  if (t.batch_streams < 1) t.batch_streams = 1;
+  const char* bk = std::getenv("HPFEM_BUBBLE_KERNEL");
+  t.bub_reg = bk && bk[0] == 'r';  // "reg" selects the register variant
+  t.hat_lb[0] = env_int("HPFEM_HAT_LB_X", 32);
+  t.hat_lb[1] = env_int("HPFEM_HAT_LB_Y", 32);
+  t.nst[0] = env_int("HPFEM_NST_X", 4);
+  t.nst[1] = env_int("HPFEM_NST_Y", 4);
+  t.eg_y = env_int("HPFEM_EG_Y", 0);
+  t.fake_stencil = env_int("HPFEM_FAKE_STENCIL", 0);
+  t.persist = env_int("HPFEM_PERSIST", 1);
+  return t;
+}
+
 /* 2D boundary code -> per-direction 1D codes (include/hpfem.h HPFEM_BC_2D) */
 bool split_bc(int bc, int& bx, int& by) {
   if (bc >= HPFEM_BC_DIRICHLET && bc <= HPFEM_BC_NEUMANN_DIRICHLET) {
@@ -328,6 +355,7 @@ struct hpfem_plan_s {
   double* wy = nullptr;           // precomputed y-solve stencil weights, J tables (table 0 unused)
   size_t wxs = 0, wys = 0;        // doubles per table
   bool use_tma = false;           // TMA half-step kernels + element-major layout
+  Tuning tun{};                   // environment switches, read once at plan time
   long long launches = 0;
   // profiling (hpfem_plan_profile)
   std::vector<cudaEvent_t> ev;
@@ -436,7 +464,7 @@ int alloc_workspace(hpfem_plan_t pl, Workspace& w, cudaStream_t st) {
     if ((ce = cudaMemsetAsync(w.Z01, 0, zb, st)) != cudaSuccess) return fail(ce, "memset workspace");
   }
   double* const arrays[3] = {w.Gp, w.X1, w.X2};
-  w.tma = tma_plan_create(pl->dx, pl->dy, pl->lay, arrays, pl->use_tma);
+  w.tma = tma_plan_create(pl->dx, pl->dy, pl->lay, arrays, pl->use_tma, pl->tun.eg_y);
   if (pl->use_tma && !tma_supports(w.tma, 0)) return fail(cudaErrorNotSupported, "TMA tensor maps");
   if (pl->use_tma) {
     if ((ce = cudaStreamCreateWithFlags(&w.hs, cudaStreamNonBlocking)) != cudaSuccess ||
@@ -486,6 +514,7 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   if (ce != cudaSuccess || ndev == 0) return set_err(HPFEM_ECUDA, "no CUDA device (no CPU fallback)");
 
   hpfem_plan_t pl = new hpfem_plan_s();
+  pl->tun = read_tuning();
   pl->hx = make_dir(xs, nx, px, bx, rob);
   pl->hy = make_dir(ys, ny, py, by, rob + 2);
   pl->omega = omega;
@@ -582,17 +611,13 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   if ((ce = cudaMemsetAsync(pl->fx, 0, sizeof(double) * pl->sx * J, st)) != cudaSuccess) return fail_cuda(ce, "memset");
   if ((ce = cudaMemsetAsync(pl->fy, 0, sizeof(double) * pl->sy * (J + 1), st)) != cudaSuccess)
     return fail_cuda(ce, "memset");
-  {
-    const char* no_tma = std::getenv("HPFEM_NO_TMA");
-    pl->use_tma = !(no_tma && no_tma[0] == '1') && tma_shape_ok(pl->dx, pl->dy);
-  }
+  pl->use_tma = !pl->tun.no_tma && tma_shape_ok(pl->dx, pl->dy, pl->tun.eg_y);
   pl->lay = make_layout(pl->dy, pl->use_tma ? 1 : 0);
   if ((rc = alloc_workspace(pl, pl->ws, st)) != HPFEM_OK) {
     free_plan(pl);
     return rc;
   }
-  const char* no_wtab = std::getenv("HPFEM_NO_WTAB");
-  if (pl->use_tma && !(no_wtab && no_wtab[0] == '1')) {  // stencil-weight tables of every ST_APPLY half-step
+  if (pl->use_tma && !pl->tun.no_wtab) {  // stencil-weight tables of every ST_APPLY half-step
     pl->wxs = tma_wtab_doubles(pl->dx, pl->dy, pl->lay, 0);
     pl->wys = tma_wtab_doubles(pl->dx, pl->dy, pl->lay, 1);
     if ((ce = cudaMalloc(&pl->wx, sizeof(double) * pl->wxs * J)) != cudaSuccess) return fail_cuda(ce, "alloc wx");
@@ -666,14 +691,9 @@ int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st,
   // Concurrent hat lines: the persistent TMA grid leaves `spare` SMs to the
   // hat-line kernel on the side stream (serial when profiling, so that the
   // per-kind times stay attributable).  HPFEM_HAT_SMS sets `spare` (0 = serial).
-  static int spare_env = -1;
-  if (spare_env < 0) {
-    const char* v = std::getenv("HPFEM_HAT_SMS");
-    spare_env = v && *v ? std::atoi(v) : 4;
-  }
-  const char* old_hl = std::getenv("HPFEM_LDG_HATLINES");
-  const bool ldg_hl = old_hl && old_hl[0] == '1';
-  if (tma_supports(w.tma, P.dir) && P.o.nh > 0 && spare_env > 0 && e0 < 0 && pl->ev.empty() && w.hs && !ldg_hl) {
+  P.tun = pl->tun;
+  const int spare_env = pl->tun.hat_sms;
+  if (tma_supports(w.tma, P.dir) && P.o.nh > 0 && spare_env > 0 && e0 < 0 && pl->ev.empty() && w.hs) {
     StepParams H = P;
     H.lp_begin = P.dir == 0 ? 0 : P.o.nb;
     H.lp_count = P.o.nh;
@@ -696,7 +716,7 @@ int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st,
     H.lp_begin = P.dir == 0 ? 0 : P.o.nb;
     H.lp_count = P.o.nh;
     if (H.lp_count > 0) {
-      rc = count_launch(pl, ldg_hl ? launch_step_bubbles(H, st) : launch_hat_lines(H, st), "hat-line kernel");
+      rc = count_launch(pl, launch_hat_lines(H, st), "hat-line kernel");
       if (rc) return rc;
       prof_add(pl, k1, e1, prof_mark(pl, st), per * (double)P.o.nh * P.s.nb);
     }
@@ -752,6 +772,15 @@ int hpfem_plan_info(hpfem_plan_t pl, int* N_x, int* N_y, int* J, double* lam_x, 
   if (lam_x) { lam_x[0] = pl->lam_x[0]; lam_x[1] = pl->lam_x[1]; }
   if (lam_y) { lam_y[0] = pl->lam_y[0]; lam_y[1] = pl->lam_y[1]; }
   if (gamma) *gamma = pl->gamma;
+  return HPFEM_OK;
+}
+
+int hpfem_plan_dims(hpfem_plan_t pl, int* n_x, int* p_x, int* n_y, int* p_y) {
+  if (!pl) return set_err(HPFEM_EINVAL, "null plan");
+  if (n_x) *n_x = pl->hx.n;
+  if (p_x) *p_x = pl->hx.p;
+  if (n_y) *n_y = pl->hy.n;
+  if (p_y) *p_y = pl->hy.p;
   return HPFEM_OK;
 }
 
@@ -853,12 +882,7 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
  * events) or with HPFEM_NO_GRAPH=1; at most kMaxGraphs cached. */
 static int solve_graph(hpfem_plan_t pl, const Workspace& w, const double* F, double* U, int iters,
                        cudaStream_t st) {
-  static int no_graph = -1;
-  if (no_graph < 0) {
-    const char* v = std::getenv("HPFEM_NO_GRAPH");
-    no_graph = v && v[0] == '1' ? 1 : 0;
-  }
-  if (no_graph || !pl->ev.empty()) return solve_core(pl, w, F, U, iters, st);
+  if (pl->tun.no_graph || !pl->ev.empty()) return solve_core(pl, w, F, U, iters, st);
   cudaError_t ce;
   for (auto& g : pl->graphs)
     if (g.w == &w && g.F == F && g.U == U && g.iters == iters) {
@@ -897,8 +921,7 @@ static int solve_graph(hpfem_plan_t pl, const Workspace& w, const double* F, dou
  * arrays fit in shared memory (HPFEM_NO_SMALL=1 disables; not while
  * profiling, so that the per-kind profile stays the multi-kernel path's) */
 static bool small_path(hpfem_plan_t pl) {
-  const char* v = std::getenv("HPFEM_NO_SMALL");
-  if (v && v[0] == '1') return false;
+  if (pl->tun.no_small) return false;
   return pl->ev.empty() && small_smem_bytes(pl->dx, pl->dy) <= SMALL_SMEM_MAX;
 }
 
@@ -953,13 +976,7 @@ int hpfem_solve_batched(hpfem_plan_t pl, int batch, const double* F, double* U, 
   if (batch == 0) return HPFEM_OK;
   if (!pl->ev.empty()) return set_err(HPFEM_EINVAL, "profiling is on: batched solves run on several streams");
   if (small_path(pl)) return solve_small(pl, batch, F, U, pl->J, st);  // one CTA per problem
-  int slots = batch;
-  {
-    const char* v = std::getenv("HPFEM_BATCH_STREAMS");
-    const int cap = v && *v ? std::atoi(v) : 8;
-    if (slots > cap) slots = cap;
-    if (slots < 1) slots = 1;
-  }
+  int slots = batch < pl->tun.batch_streams ? batch : pl->tun.batch_streams;
   cudaError_t ce;
   while ((int)pl->bws.size() < slots) {  // stream slots, each with its own buffers
     Workspace w;

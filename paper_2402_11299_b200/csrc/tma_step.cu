@@ -650,14 +650,14 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
+  static const EncodeTiledFn fn = [] {  // thread-safe one-time initialisation
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (EncodeTiledFn)p;
-  }
+      return (EncodeTiledFn)p;
+    return (EncodeTiledFn) nullptr;
+  }();
   return fn;
 }
 
@@ -693,11 +693,6 @@ static int even_up(int v) { return (v + 1) & ~1; }
 /* y-solve tile shape: EG y-elements (a power of two <= 8, so that a warp
  * holds whole rows: RW = 16/EG rows per warp) x R rows of an x-chain (a
  * multiple of RW, with the R+2-row W box inside each parity's row count) */
-static int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atoi(v) : dflt;
-}
-
 static void y_tile_shape_eg(const DirDev& x, const DirDev& y, int eg, int& EG, int& R) {
   EG = eg;
   while (EG > y.n) EG >>= 1;
@@ -709,8 +704,7 @@ static void y_tile_shape_eg(const DirDev& x, const DirDev& y, int eg, int& EG, i
 
 /* choose EG in {4, 8}: fewest idle rows in the x-chain windows, then the
  * larger window (W rows reused R/(R+2)); HPFEM_EG_Y overrides */
-static void y_tile_shape(const DirDev& x, const DirDev& y, int& EG, int& R) {
-  const int forced = env_int("HPFEM_EG_Y", 0);
+static void y_tile_shape(const DirDev& x, const DirDev& y, int forced, int& EG, int& R) {
   if (forced) {
     y_tile_shape_eg(x, y, forced, EG, R);
     return;
@@ -732,17 +726,18 @@ static void y_tile_shape(const DirDev& x, const DirDev& y, int& EG, int& R) {
 }
 
 /* shape conditions of the TMA path (both directions, element-major layout) */
-bool tma_shape_ok(const DirDev& x, const DirDev& y) {
+bool tma_shape_ok(const DirDev& x, const DirDev& y, int eg_y) {
   const int Q = even_up(y.p - 1);
   int EG, R;
-  y_tile_shape(x, y, EG, R);
+  y_tile_shape(x, y, eg_y, EG, R);
   return x.nb > 0 && y.nb > 0 && x.N >= 2 && Q <= 256 && Q >= KBOX && chain_len(x.p, 0) <= 64 &&
          chain_len(y.p, 0) <= 64 && R >= 16 / EG;
 }
 
-TmaPlan* tma_plan_create(const DirDev& x, const DirDev& y, const Layout& L, double* const arrays[3], int enable) {
+TmaPlan* tma_plan_create(const DirDev& x, const DirDev& y, const Layout& L, double* const arrays[3], int enable,
+                         int eg_y) {
   TmaPlan* T = new TmaPlan();
-  if (!enable || !L.emaj || !encode_fn() || !tma_shape_ok(x, y)) return T;
+  if (!enable || !L.emaj || !encode_fn() || !tma_shape_ok(x, y, eg_y)) return T;
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&T->sms, cudaDevAttrMultiProcessorCount, dev);
@@ -775,7 +770,7 @@ TmaPlan* tma_plan_create(const DirDev& x, const DirDev& y, const Layout& L, doub
   // ---- y-solve views
   {
     int EG, R;
-    y_tile_shape(x, y, EG, R);
+    y_tile_shape(x, y, eg_y, EG, R);
     const int RW = 16 / EG;
     T->EG1 = EG;
     T->R = R;
@@ -810,25 +805,13 @@ void tma_plan_destroy(TmaPlan* T) { delete T; }
 
 bool tma_supports(const TmaPlan* T, int dir) { return T && T->ok && (dir == 0 || dir == 1); }
 
-/* The dynamic shared-memory opt-in is set once per kernel instantiation:
- * cudaFuncSetAttribute can serialise with in-flight launches of the same
- * kernel, which would stall the host between half-steps. */
 constexpr int SMEM_OPTIN = 227 * 1024;  // the sm_100 per-CTA maximum
-
-template <typename K>
-static cudaError_t optin(K k, bool& done) {
-  if (done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_OPTIN);
-  if (e == cudaSuccess) done = true;
-  return e;
-}
 
 template <int CL, int MODE>
 static cudaError_t launch_x(const TmaStepArgs& A, const CUtensorMap* g, const CUtensorMap* w, int grid, size_t smem,
                             cudaStream_t st) {
   auto k = k_xstep_tma<CL, MODE>;
-  static bool done = false;
-  cudaError_t e = optin(k, done);
+  cudaError_t e = smem_optin((const void*)k, SMEM_OPTIN);  // once per (kernel, device)
   if (e != cudaSuccess) return e;
   k<<<grid, NT, smem, st>>>(A, g[0], g[1], w[0], w[1], w[2], w[3]);
   return cudaGetLastError();
@@ -838,8 +821,7 @@ template <int CL, int MODE>
 static cudaError_t launch_y(const TmaStepArgs& A, const TmaPlan* T, int gi, int wi, int grid, size_t smem,
                             cudaStream_t st) {
   auto k = k_ystep_tma<CL, MODE>;
-  static bool done = false;
-  cudaError_t e = optin(k, done);
+  cudaError_t e = smem_optin((const void*)k, SMEM_OPTIN);
   if (e != cudaSuccess) return e;
   k<<<grid, NT, smem, st>>>(A, T->yG[gi][0], T->yG[gi][1], T->yW[wi][0], T->yW[wi][1], T->yH[wi], T->yO[0],
                             T->yO[1]);
@@ -875,7 +857,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
   TmaStepArgs A;
   std::memset(&A, 0, sizeof(A));
   A.P = P;
-  A.fake_stencil = env_int("HPFEM_FAKE_STENCIL", 0);
+  A.fake_stencil = P.tun.fake_stencil;
   const int gi = ia_g >= 0 ? ia_g : ia_w, wi = ia_w >= 0 ? ia_w : ia_g;
   const int budget = SMEM_OPTIN - 4096;
   if (P.dir == 0) {
@@ -895,7 +877,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
     A.wb_doubles = P.wtab ? A.EG * 5 * P.lay.Q : 0;
     A.S = (chain_len(x.p, 0) - 1) / KR + 1;
     A.nstages = (budget - 2 * A.fac_doubles * 8 - 2 * A.wb_doubles * 8) / A.stage_bytes;
-    if (A.nstages > env_int("HPFEM_NST_X", 4)) A.nstages = env_int("HPFEM_NST_X", 4);  // 4 measured best
+    if (A.nstages > P.tun.nst[0]) A.nstages = P.tun.nst[0];  // 4 measured best
     if (A.nstages > A.S) A.nstages = A.S;  // the factor double buffer relies on NST <= S
     if (A.nstages < 1) A.nstages = 1;
     A.fac_off = A.nstages * A.stage_bytes;
@@ -934,7 +916,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
   A.wb_doubles = P.wtab ? ((A.R * 6 + 15) & ~15) : 0;
   A.S = (chain_len(y.p, 0) - 1) / KCP + 1;
   A.nstages = (budget - obytes - 2 * A.fac_doubles * 8 - 2 * A.wb_doubles * 8) / A.stage_bytes;
-  if (A.nstages > env_int("HPFEM_NST_Y", 4)) A.nstages = env_int("HPFEM_NST_Y", 4);
+  if (A.nstages > P.tun.nst[1]) A.nstages = P.tun.nst[1];
   if (A.nstages > A.S) A.nstages = A.S;  // see x-solve
   if (A.nstages < 1) A.nstages = 1;
   A.out_off = A.nstages * A.stage_bytes;

@@ -14,10 +14,11 @@ namespace hpfem {
 struct TmaPlan;
 
 /* shape conditions of the TMA path (it then needs the element-major layout) */
-bool tma_shape_ok(const DirDev& x, const DirDev& y);
+bool tma_shape_ok(const DirDev& x, const DirDev& y, int eg_y = 0);  // eg_y: Tuning::eg_y
 
 /* arrays = {Gp, X1, X2} (internal layout L); enable = 0 disables the path */
-TmaPlan* tma_plan_create(const DirDev& x, const DirDev& y, const Layout& L, double* const arrays[3], int enable);
+TmaPlan* tma_plan_create(const DirDev& x, const DirDev& y, const Layout& L, double* const arrays[3], int enable,
+                         int eg_y = 0);
 void tma_plan_destroy(TmaPlan* T);
 /* can the TMA kernel handle the bubble lines of a solve along dir? */
 bool tma_supports(const TmaPlan* T, int dir);

@@ -108,3 +108,17 @@ def test_boundary_codes_validated_before_device():
         assert rc(bc, 0.0) == -1, bc  # a Neumann-only direction needs w != 0
     for bc in (-1, 4, 15, 32, hp.HPFEM_BC_2D(0, 4)):
         assert rc(bc, 1.0) == -1, bc
+
+
+def test_binding_checks_sizes():
+    """The binding refuses a buffer of the wrong size before the C ABI sees
+    the raw pointer (an undersized buffer would be read / written past its
+    end).  No device needed: the size check comes first."""
+    import pytest
+    import torch
+
+    import paper_2402_11299_b200 as hp
+
+    with pytest.raises(ValueError):
+        hp._sized(torch.zeros(3, dtype=torch.float64), 4, "F")
+    assert hp._sized(12345, 4, "F") == 12345  # raw pointers pass unchecked
