@@ -130,6 +130,7 @@ struct Tuning {
   int eg_y;           // HPFEM_EG_Y (0 = automatic): y-solve tile width
   int fake_stencil;   // HPFEM_FAKE_STENCIL (0): experiment only
   int persist;        // HPFEM_PERSIST (1): persistent one-launch solve for L2-resident problems
+  int hats_seq;       // HPFEM_HATS_SEQ (0): the sequential one-thread-per-line hat Schur kernel (experiment / A-B)
 };
 
 /* Raise a kernel's dynamic shared-memory limit to `bytes` on the CURRENT

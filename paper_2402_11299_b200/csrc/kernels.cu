@@ -1022,9 +1022,275 @@ cudaError_t launch_hat_lines(const StepParams& P, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+/* ------------------------------------------------------------------ */
+/* K5, parallel form: the hat Schur solves with every thread busy.     */
+/* The hat factor is the reverse Cholesky of the hat Schur complement   */
+/* (Alg. 1 line 7 / R3): two first-order linear recurrences per line,  */
+/*   y_t = il_t r_t - hd_t y_{t+1}   (t = nh-1 .. 0),                   */
+/*   x_t = il_t y_t - hu_t x_{t-1}   (t = 0 .. nh-1),                   */
+/* hd_t = g_t il_t, hu_t = g_{t-1} il_t.  A recurrence over a block of  */
+/* hats is an affine map of the value entering the block; the maps of   */
+/* the blocks are combined by a scan (warp shuffles / a shared-memory   */
+/* fold) and every block then sweeps locally -- O(nh / P + log P) steps */
+/* instead of nh (north_star K1: PCR / cyclic-reduction class).  Same   */
+/* factors, same right-hand sides; only the association of the products */
+/* differs from the sequential sweep (rounding-level, checked against   */
+/* the oracle's rounding floor in tests/test_gpu_parity.py).            */
+/* ------------------------------------------------------------------ */
+struct Aff {  // y = a + b * y_in
+  double a, b;
+};
+
+__device__ __forceinline__ Aff aff_after(const Aff& f, const Aff& g) {  // f o g
+  return Aff{fma(f.b, g.a, f.a), f.b * g.b};
+}
+
+/* per-hat tables of a hat Schur CTA: il, hd, hu, and the couplings
+ * B(h, W_0 / W_1) of the left / right element (0 where absent) */
+__device__ __forceinline__ void hat_tables(const StepParams& P, double* fil, double* fhd, double* fhu, double* cpl) {
+  const DirDev& s = P.s;
+  const double S = P.f.sig;
+  const bool k1 = s.p - 2 >= 1;
+  for (int t = threadIdx.x; t < s.nh; t += blockDim.x) {
+    const double il = __ldg(P.f.ilh + t);
+    fil[t] = il;
+    fhd[t] = __ldg(P.f.gh + t) * il;
+    fhu[t] = (t > 0 ? __ldg(P.f.gh + t - 1) : 0.0) * il;
+    const int node = node_of_hat(t, s.bc);
+    const int eL = node - 1, eR = node;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    if (eL >= 0) {
+      const double dl = s.delta[eL];
+      c0 = s_hat_bub(S, dl, 1, 0);
+      if (k1) c1 = s_hat_bub(S, dl, 1, 1);
+    }
+    if (eR <= s.n - 1) {
+      const double dr = s.delta[eR];
+      c2 = s_hat_bub(S, dr, 0, 0);
+      if (k1) c3 = s_hat_bub(S, dr, 0, 1);
+    }
+    cpl[4 * t] = c0;
+    cpl[4 * t + 1] = c1;
+    cpl[4 * t + 2] = c2;
+    cpl[4 * t + 3] = c3;
+  }
+}
+
+/* y-solves (DIR 1): lines = rows, one warp per row, lane L owns the hats
+ * [L HB, L HB + HB) (contiguous in the row: coalesced loads / stores) */
+template <int HB>
+__global__ void __launch_bounds__(256, 2) k_hats_rows(StepParams P) {
+  __shared__ double fil[256], fhd[256], fhu[256], cpl[4 * 256];
+  const DirDev& s = P.s;
+  const int nh = s.nh, n = s.n, ld = P.ld, dl = drop_left(s.bc);
+  const int lane = threadIdx.x & 31;
+  const int t0 = lane * HB;
+  const bool k1 = s.p - 2 >= 1;
+  hat_tables(P, fil, fhd, fhu, cpl);
+  __syncthreads();
+  const double* __restrict__ G = P.G;
+  const double* __restrict__ Xp = P.Xp;
+  const double aG = P.alphaG;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int lp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; lp < P.o.N; lp += nwarps) {
+    const int l = row_of(P.o, lp);
+    Stencil st;
+    line_stencil<1>(P, l, st);
+    // chain-first bubbles z(l, e, 0/1) of the elements e = t0 + dl - 1 .. t0 + dl + HB - 1
+    double2 zz[HB + 1];
+#pragma unroll
+    for (int i = 0; i <= HB; ++i) {
+      int e = t0 + dl - 1 + i;
+      e = e < 0 ? 0 : (e > n - 1 ? n - 1 : e);  // absent elements have zero couplings
+      if (P.z01) {
+        zz[i] = __ldg(reinterpret_cast<const double2*>(P.z01 + (size_t)l * 2 * n + 2 * e));
+      } else {
+        zz[i].x = __ldg(P.out + (size_t)l * ld + ycol_ke(P.lay, 0, e));
+        zz[i].y = k1 ? __ldg(P.out + (size_t)l * ld + ycol_ke(P.lay, 1, e)) : 0.0;
+      }
+    }
+    double r[HB];
+#pragma unroll
+    for (int i = 0; i < HB; ++i) {
+      const int t = t0 + i;
+      double rh = 0.0;
+      if (t < nh) {
+        if (aG != 0.0) rh = aG * __ldg(G + (size_t)l * ld + t);
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+          if (st.idx[q] >= 0) rh += st.w[q] * __ldg(Xp + (size_t)st.idx[q] * ld + t);
+        const double* c = cpl + 4 * t;
+        rh -= c[0] * zz[i].x;
+        if (k1) rh -= c[1] * zz[i].y;
+        rh -= c[2] * zz[i + 1].x;
+        if (k1) rh -= c[3] * zz[i + 1].y;
+      }
+      r[i] = rh;
+    }
+    // down sweep: block map, suffix scan over the lanes, local sweep
+    Aff f{0.0, 1.0};
+#pragma unroll
+    for (int i = HB - 1; i >= 0; --i) {
+      const int t = t0 + i;
+      if (t < nh) f = Aff{fma(-fhd[t], f.a, fil[t] * r[i]), -fhd[t] * f.b};
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      Aff g{__shfl_down_sync(0xffffffffu, f.a, d), __shfl_down_sync(0xffffffffu, f.b, d)};
+      if (lane + d < 32) f = aff_after(f, g);
+    }
+    double v = __shfl_down_sync(0xffffffffu, f.a, 1);
+    if (lane == 31) v = 0.0;
+#pragma unroll
+    for (int i = HB - 1; i >= 0; --i) {
+      const int t = t0 + i;
+      if (t < nh) {
+        v = fma(-fhd[t], v, fil[t] * r[i]);
+        r[i] = v;
+      }
+    }
+    // up sweep: block map, prefix scan, local sweep and store
+    f = Aff{0.0, 1.0};
+#pragma unroll
+    for (int i = 0; i < HB; ++i) {
+      const int t = t0 + i;
+      if (t < nh) f = Aff{fma(-fhu[t], f.a, fil[t] * r[i]), -fhu[t] * f.b};
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      Aff g{__shfl_up_sync(0xffffffffu, f.a, d), __shfl_up_sync(0xffffffffu, f.b, d)};
+      if (lane >= d) f = aff_after(f, g);
+    }
+    v = __shfl_up_sync(0xffffffffu, f.a, 1);
+    if (lane == 0) v = 0.0;
+    double* __restrict__ out = P.out + (size_t)l * ld;
+#pragma unroll
+    for (int i = 0; i < HB; ++i) {
+      const int t = t0 + i;
+      if (t < nh) {
+        v = fma(-fhu[t], v, fil[t] * r[i]);
+        out[t] = v;
+      }
+    }
+  }
+}
+
+/* x-solves (DIR 0): lines = internal columns, lane = column (coalesced),
+ * the 8 warps of a CTA split each column's hats into 8 blocks; the block
+ * maps are folded through shared memory */
+constexpr int HC_COLS = 32;
+__host__ __device__ constexpr size_t hats_cols_smem_doubles(int nh) {
+  return (size_t)nh * HC_COLS + 7 * (size_t)nh + 2 * 8 * HC_COLS;
+}
+
+__global__ void __launch_bounds__(256, 4) k_hats_cols(StepParams P) {
+  extern __shared__ double sh[];
+  const DirDev& s = P.s;
+  const int nh = s.nh, n = s.n, ld = P.ld, dl = drop_left(s.bc);
+  const bool k1 = s.p - 2 >= 1;
+  double* v = sh;                          // [nh][32]: r, then y, per column
+  double* fil = v + (size_t)nh * HC_COLS;
+  double* fhd = fil + nh;
+  double* fhu = fhd + nh;
+  double* cpl = fhu + nh;                  // [nh][4]
+  double* fa = cpl + 4 * nh;               // [8][32] block maps
+  double* fb = fa + 8 * HC_COLS;
+  hat_tables(P, fil, fhd, fhu, cpl);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int li = blockIdx.x * HC_COLS + lane;
+  const int l = li < ld ? ydof_of_col(P.lay, P.o, li) : -1;
+  const int BH = (nh + 7) >> 3;
+  const int ta = w * BH, tb = min(nh, ta + BH);
+  __syncthreads();
+  if (l >= 0) {
+    Stencil st;
+    line_stencil<0>(P, l, st);
+    const double* __restrict__ G = P.G;
+    const double* __restrict__ Xp = P.Xp;
+    const double* __restrict__ Z = P.out;  // chain-first bubbles of this half-step
+    const double aG = P.alphaG;
+#pragma unroll 4
+    for (int t = ta; t < tb; ++t) {
+      const int node = t + dl;
+      const int eL = max(node - 1, 0), eR = min(node, n - 1);  // absent: zero coupling
+      const double zl0 = __ldg(Z + (size_t)(s.nh + eL) * ld + li);
+      const double zr0 = __ldg(Z + (size_t)(s.nh + eR) * ld + li);
+      const double zl1 = k1 ? __ldg(Z + (size_t)(s.nh + n + eL) * ld + li) : 0.0;
+      const double zr1 = k1 ? __ldg(Z + (size_t)(s.nh + n + eR) * ld + li) : 0.0;
+      double rh = aG != 0.0 ? aG * __ldg(G + (size_t)t * ld + li) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 7; ++q)
+        if (st.idx[q] >= 0) rh += st.w[q] * __ldg(Xp + (size_t)t * ld + st.idx[q]);
+      const double* c = cpl + 4 * t;
+      rh -= c[0] * zl0;
+      if (k1) rh -= c[1] * zl1;
+      rh -= c[2] * zr0;
+      if (k1) rh -= c[3] * zr1;
+      v[t * HC_COLS + lane] = rh;
+    }
+  }
+  // down sweep
+  Aff f{0.0, 1.0};
+  for (int t = tb - 1; t >= ta; --t) f = Aff{fma(-fhd[t], f.a, fil[t] * v[t * HC_COLS + lane]), -fhd[t] * f.b};
+  fa[w * HC_COLS + lane] = f.a;
+  fb[w * HC_COLS + lane] = f.b;
+  __syncthreads();
+  double y = 0.0;
+  for (int u = 7; u > w; --u) y = fma(fb[u * HC_COLS + lane], y, fa[u * HC_COLS + lane]);
+  for (int t = tb - 1; t >= ta; --t) {
+    y = fma(-fhd[t], y, fil[t] * v[t * HC_COLS + lane]);
+    v[t * HC_COLS + lane] = y;
+  }
+  f = Aff{0.0, 1.0};
+  for (int t = ta; t < tb; ++t) f = Aff{fma(-fhu[t], f.a, fil[t] * v[t * HC_COLS + lane]), -fhu[t] * f.b};
+  __syncthreads();  // every y of the block is written and the down-sweep maps are read
+  fa[w * HC_COLS + lane] = f.a;
+  fb[w * HC_COLS + lane] = f.b;
+  __syncthreads();
+  double x = 0.0;
+  for (int u = 0; u < w; ++u) x = fma(fb[u * HC_COLS + lane], x, fa[u * HC_COLS + lane]);
+  if (l >= 0)
+    for (int t = ta; t < tb; ++t) {
+      x = fma(-fhu[t], x, fil[t] * v[t * HC_COLS + lane]);
+      P.out[(size_t)t * ld + li] = x;
+    }
+}
+
+template <int HB>
+static cudaError_t launch_hats_rows(const StepParams& P, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int warps = P.o.N, blocks = (warps + 7) / 8;
+  const int grid = blocks < 2 * sms ? blocks : 2 * sms;  // one wave of 2 CTAs per SM, grid-stride over rows
+  k_hats_rows<HB><<<grid, 256, 0, st>>>(P);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st) {
   if (P.s.nh == 0) return cudaSuccess;
-  return P.dir == 0 ? launch_hats_dir<0>(P, st) : launch_hats_dir<1>(P, st);
+  if (P.tun.hats_seq) return P.dir == 0 ? launch_hats_dir<0>(P, st) : launch_hats_dir<1>(P, st);  // experiment
+  const int nh = P.s.nh;
+  if (P.dir == 1 && nh <= 256) {
+    switch ((nh + 31) / 32) {
+      case 1: return launch_hats_rows<1>(P, st);
+      case 2: return launch_hats_rows<2>(P, st);
+      case 3: return launch_hats_rows<3>(P, st);
+      case 4: return launch_hats_rows<4>(P, st);
+      case 5: return launch_hats_rows<5>(P, st);
+      case 6: return launch_hats_rows<6>(P, st);
+      case 7: return launch_hats_rows<7>(P, st);
+      default: return launch_hats_rows<8>(P, st);
+    }
+  }
+  const size_t smem = sizeof(double) * hats_cols_smem_doubles(nh);
+  if (P.dir == 0 && smem <= 200 * 1024) {
+    cudaError_t e = smem_optin((const void*)k_hats_cols, smem);
+    if (e != cudaSuccess) return e;
+    k_hats_cols<<<(P.ld + HC_COLS - 1) / HC_COLS, 256, smem, st>>>(P);
+    return cudaGetLastError();
+  }
+  return P.dir == 0 ? launch_hats_dir<0>(P, st) : launch_hats_dir<1>(P, st);  // very many hats
 }
 
 /* K6: U = W_J C^{-1} materialised in the caller's layout:

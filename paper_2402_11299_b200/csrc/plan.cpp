@@ -21,6 +21,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: no-ops unless a profiler injects itself
+
 #include "../../include/hpfem.h"
 #include "hpfem_internal.h"
 #include "ops1d.h"
@@ -29,6 +31,15 @@
 using namespace hpfem;
 
 namespace {
+
+/* NVTX range for the host-side enqueue of one stage of the solve (visible in
+ * nsys / ncu --nvtx timelines; one range per half-step of Alg. 2) */
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 thread_local std::string t_err;
 
@@ -65,6 +76,7 @@ Tuning read_tuning() {
   t.eg_y = env_int("HPFEM_EG_Y", 0);
   t.fake_stencil = env_int("HPFEM_FAKE_STENCIL", 0);
   t.persist = env_int("HPFEM_PERSIST", 1);
+  t.hats_seq = env_int("HPFEM_HATS_SEQ", 0);
   return t;
 }
 
@@ -817,6 +829,7 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
     P.lp_count = P.o.N;
     return P;
   };
+  NvtxRange solve_range("hpfem_solve");
   for (int j = 0; j < iters; ++j) {
     // half-step A: W_{j-1/2} = (G - (A_x - p_j M_x) W_{j-1}) (A_y + p_j M_y)^{-1}
     StepParams A = base(1);
@@ -837,7 +850,10 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
       A.cvR = prev.vR;
       if (pl->wy) A.wtab = pl->wy + pl->wys * j;
     }
-    if ((rc = run_step(pl, w, A, st, false, 0, j == 0 ? -1 : 2))) return rc;
+    {
+      NvtxRange r("ADI half-step A (y-solves)");
+      if ((rc = run_step(pl, w, A, st, false, 0, j == 0 ? -1 : 2))) return rc;
+    }
     // half-step B: W_j = (A_x - q_j M_x)^{-1} (G - W_{j-1/2} (A_y + q_j M_y))
     StepParams B = base(0);
     B.G = w.Gp;
@@ -852,9 +868,13 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
     B.cvL = A.f.vL;
     B.cvR = A.f.vR;
     if (pl->wx) B.wtab = pl->wx + pl->wxs * j;
-    if ((rc = run_step(pl, w, B, st, false, 0, 1))) return rc;
+    {
+      NvtxRange r("ADI half-step B (x-solves)");
+      if ((rc = run_step(pl, w, B, st, false, 0, 1))) return rc;
+    }
   }
   // RETURN W_J C^{-1}: y-solves with the mass factor, then materialise U
+  NvtxRange rf("final W_J C^-1");
   StepParams Fin = base(1);
   Fin.G = nullptr;
   Fin.alphaG = 0.0;

@@ -396,7 +396,7 @@ __device__ __forceinline__ void y_issue(const TmaStepArgs& A, uint32_t gs, unsig
   }
 }
 
-template <int CL, int MODE>
+template <int CL, int MODE, int EGT>
 __global__ void __launch_bounds__(NT, 1)
     k_ystep_tma(const TmaStepArgs A, const __grid_constant__ CUtensorMap mG0, const __grid_constant__ CUtensorMap mG1,
                 const __grid_constant__ CUtensorMap mW0, const __grid_constant__ CUtensorMap mW1,
@@ -413,7 +413,11 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.bar_off);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(full + NST);
   const int lane = threadIdx.x & 31;
-  const int EG = A.EG, R = A.R;
+  // EGT: the tile width as a compile-time constant, so that the swizzled box
+  // addresses of the 6 stencil rows differ by immediates (one XOR per
+  // position instead of one per row: the y kernel was address-ALU heavy)
+  constexpr int EG = EGT;
+  const int R = A.R;
   const int my = chain_len(y.p, 0);
   if (threadIdx.x < NST) cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
@@ -817,10 +821,10 @@ static cudaError_t launch_x(const TmaStepArgs& A, const CUtensorMap* g, const CU
   return cudaGetLastError();
 }
 
-template <int CL, int MODE>
+template <int CL, int MODE, int EGT>
 static cudaError_t launch_y(const TmaStepArgs& A, const TmaPlan* T, int gi, int wi, int grid, size_t smem,
                             cudaStream_t st) {
-  auto k = k_ystep_tma<CL, MODE>;
+  auto k = k_ystep_tma<CL, MODE, EGT>;
   cudaError_t e = smem_optin((const void*)k, SMEM_OPTIN);
   if (e != cudaSuccess) return e;
   k<<<grid, NT, smem, st>>>(A, T->yG[gi][0], T->yG[gi][1], T->yW[wi][0], T->yW[wi][1], T->yH[wi], T->yO[0],
@@ -837,13 +841,24 @@ static cudaError_t dispatch_x(int cl, const TmaStepArgs& A, const CUtensorMap* g
   return launch_x<64, MODE>(A, g, w, grid, smem, st);
 }
 
+template <int MODE, int EGT>
+static cudaError_t dispatch_y_eg(int cl, const TmaStepArgs& A, const TmaPlan* T, int gi, int wi, int grid,
+                                 size_t smem, cudaStream_t st) {
+  if (cl <= 8) return launch_y<8, MODE, EGT>(A, T, gi, wi, grid, smem, st);
+  if (cl <= 16) return launch_y<16, MODE, EGT>(A, T, gi, wi, grid, smem, st);
+  if (cl <= 32) return launch_y<32, MODE, EGT>(A, T, gi, wi, grid, smem, st);
+  return launch_y<64, MODE, EGT>(A, T, gi, wi, grid, smem, st);
+}
+
 template <int MODE>
 static cudaError_t dispatch_y(int cl, const TmaStepArgs& A, const TmaPlan* T, int gi, int wi, int grid, size_t smem,
                               cudaStream_t st) {
-  if (cl <= 8) return launch_y<8, MODE>(A, T, gi, wi, grid, smem, st);
-  if (cl <= 16) return launch_y<16, MODE>(A, T, gi, wi, grid, smem, st);
-  if (cl <= 32) return launch_y<32, MODE>(A, T, gi, wi, grid, smem, st);
-  return launch_y<64, MODE>(A, T, gi, wi, grid, smem, st);
+  switch (A.EG) {  // y_tile_shape: a power of two <= 8
+    case 8: return dispatch_y_eg<MODE, 8>(cl, A, T, gi, wi, grid, smem, st);
+    case 4: return dispatch_y_eg<MODE, 4>(cl, A, T, gi, wi, grid, smem, st);
+    case 2: return dispatch_y_eg<MODE, 2>(cl, A, T, gi, wi, grid, smem, st);
+    default: return dispatch_y_eg<MODE, 1>(cl, A, T, gi, wi, grid, smem, st);
+  }
 }
 
 static int round128(int b) { return (b + 127) & ~127; }
