@@ -113,6 +113,15 @@ int hpfem_plan_info(hpfem_plan_t plan, int* N_x, int* N_y, int* J, double* lam_x
  * pointers and cannot). */
 int hpfem_plan_dims(hpfem_plan_t plan, int* n_x, int* p_x, int* n_y, int* p_y);
 
+/* Kernel path of hpfem_solve for this plan (host outputs; either may be
+ * NULL): *path = 0 one-CTA-per-problem solve (K11, arrays in shared
+ * memory), 1 TMA half-step kernels, 2 LDG half-step kernels;
+ * *transposed = 1 when the plan runs Alg. 2 on the transposed equation
+ * A_y U^T M_x + M_y U^T A_x = G^T (the long bubble chains then lie along the
+ * rows of the internal arrays; reading R23) -- same J, the shifts
+ * of the swapped intervals, U returned in the caller's layout. */
+int hpfem_plan_path(hpfem_plan_t plan, int* path, int* transposed);
+
 /* Host copies of the shifts: p[0..J-1] (used by the y-solves and the
  * x-applies), q[0..J-1] (x-solves and y-applies), ascending j. */
 int hpfem_plan_shifts(hpfem_plan_t plan, double* p, double* q);

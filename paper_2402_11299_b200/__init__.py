@@ -55,6 +55,7 @@ def _load():
     L.hpfem_plan_info.argtypes = [_vp, _ip, _ip, _ip, _dp, _dp, _dp]
     L.hpfem_plan_shifts.argtypes = [_vp, _dp, _dp]
     L.hpfem_plan_dims.argtypes = [_vp, _ip, _ip, _ip, _ip]
+    L.hpfem_plan_path.argtypes = [_vp, _ip, _ip]
     L.hpfem_solve.argtypes = [_vp, _vp, _vp, _vp]
     L.hpfem_solve_iters.argtypes = [_vp, _vp, _vp, _i, _vp]
     L.hpfem_apply.argtypes = [_vp, _vp, _vp, _vp]
@@ -77,7 +78,7 @@ def _load():
     L.hpfem_plan_destroy.argtypes = [_vp]
     L.hpfem_plan_destroy.restype = None
     L.hpfem_last_error.restype = ctypes.c_char_p
-    for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_dims", "hpfem_plan_shifts", "hpfem_solve",
+    for f in ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_dims", "hpfem_plan_path", "hpfem_plan_shifts", "hpfem_solve",
               "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
               "hpfem_plan_profile_read", "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_grid",
               "hpfem_transform", "hpfem_itransform", "hpfem_varcoef_apply", "hpfem_pcg", "hpfem_imex_step"):
@@ -86,7 +87,7 @@ def _load():
     return L
 
 
-EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_dims", "hpfem_plan_shifts", "hpfem_solve",
+EXPORTS = ("hpfem_plan", "hpfem_plan_mesh", "hpfem_plan_robin", "hpfem_plan_info", "hpfem_plan_dims", "hpfem_plan_path", "hpfem_plan_shifts", "hpfem_solve",
            "hpfem_solve_iters", "hpfem_solve_batched", "hpfem_apply", "hpfem_load", "hpfem_unload", "hpfem_plan_launches", "hpfem_plan_profile",
            "hpfem_plan_profile_read", "hpfem_plan_destroy", "hpfem_last_error",
            "hpfem_plan1d", "hpfem_plan1d_info", "hpfem_solve1d", "hpfem_plan1d_destroy",
@@ -180,6 +181,13 @@ def hpfem_plan_dims(plan: int) -> dict:
     nx, px, ny, py = _i(), _i(), _i(), _i()
     _check(_load().hpfem_plan_dims(plan, ctypes.byref(nx), ctypes.byref(px), ctypes.byref(ny), ctypes.byref(py)))
     return dict(nx=nx.value, px=px.value, ny=ny.value, py=py.value)
+
+
+def hpfem_plan_path(plan: int) -> dict:
+    """{"path": "small" | "tma" | "ldg", "transposed": bool}"""
+    path, tr = _i(), _i()
+    _check(_load().hpfem_plan_path(plan, ctypes.byref(path), ctypes.byref(tr)))
+    return dict(path=("small", "tma", "ldg")[path.value], transposed=bool(tr.value))
 
 
 def _nn(plan: int) -> int:
@@ -362,6 +370,9 @@ class Plan:
 
     def shifts(self):
         return hpfem_plan_shifts(self.handle)
+
+    def path(self) -> dict:
+        return hpfem_plan_path(self.handle)
 
     def solve(self, F, U, stream=None, iters=None):
         if iters is None:

@@ -131,6 +131,7 @@ struct Tuning {
   int fake_stencil;   // HPFEM_FAKE_STENCIL (0): experiment only
   int persist;        // HPFEM_PERSIST (1): persistent one-launch solve for L2-resident problems
   int hats_seq;       // HPFEM_HATS_SEQ (0): the sequential one-thread-per-line hat Schur kernel (experiment / A-B)
+  int transpose;      // HPFEM_TRANSPOSE (-1 auto, 0 never, 1 always): solve the transposed equation (R23)
 };
 
 /* Raise a kernel's dynamic shared-memory limit to `bytes` on the CURRENT
@@ -181,6 +182,8 @@ cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st);
 cudaError_t launch_hat_lines(const StepParams& P, cudaStream_t st);  // element-major layout only
 cudaError_t launch_copyin(const DirDev& x, const DirDev& y, const Layout& L, const double* G, double* Gp,
                           cudaStream_t st);
+/* out (C x R) = in (R x C)^T, both row-major and contiguous */
+cudaError_t launch_transpose(const double* in, int R, int C, double* out, cudaStream_t st);
 cudaError_t launch_finalize(const DirDev& x, const DirDev& y, const Layout& L, const double* vL, const double* vR,
                             const double* X, double* U, cudaStream_t st);
 cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const double* U, double* F,

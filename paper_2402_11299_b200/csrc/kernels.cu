@@ -1386,6 +1386,32 @@ cudaError_t launch_finalize(const DirDev& x, const DirDev& y, const Layout& L, c
   return cudaGetLastError();
 }
 
+/* plain transpose through 32 x 33 shared-memory tiles (coalesced both ways):
+ * out[c][r] = in[r][c]; the transposed solve's copy-in / finalize (R23) */
+__global__ void __launch_bounds__(256) k_transpose(const double* __restrict__ in, int R, int C,
+                                                   double* __restrict__ out) {
+  __shared__ double t[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32, tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int r = r0 + rr, c = c0 + tx;
+    if (r < R && c < C) t[rr][tx] = __ldg(in + (size_t)r * C + c);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int cc = ty; cc < 32; cc += 8) {
+    const int c = c0 + cc, r = r0 + tx;
+    if (r < R && c < C) out[(size_t)c * R + r] = t[tx][cc];
+  }
+}
+
+cudaError_t launch_transpose(const double* in, int R, int C, double* out, cudaStream_t st) {
+  if (R <= 0 || C <= 0) return cudaSuccess;
+  dim3 grid((C + 31) / 32, (R + 31) / 32);
+  k_transpose<<<grid, dim3(32, 8), 0, st>>>(in, R, C, out);
+  return cudaGetLastError();
+}
+
 /* G (caller layout) -> Gp (internal layout) */
 __global__ void __launch_bounds__(256) k_copyin(DirDev y, int Nx, Layout L, const double* __restrict__ G,
                                                  double* __restrict__ Gp) {

@@ -77,6 +77,7 @@ Tuning read_tuning() {
   t.fake_stencil = env_int("HPFEM_FAKE_STENCIL", 0);
   t.persist = env_int("HPFEM_PERSIST", 1);
   t.hats_seq = env_int("HPFEM_HATS_SEQ", 0);
+  t.transpose = env_int("HPFEM_TRANSPOSE", -1);
   return t;
 }
 
@@ -367,6 +368,18 @@ struct hpfem_plan_s {
   double* wy = nullptr;           // precomputed y-solve stencil weights, J tables (table 0 unused)
   size_t wxs = 0, wys = 0;        // doubles per table
   bool use_tma = false;           // TMA half-step kernels + element-major layout
+  /* Solve orientation.  Alg. 2 is symmetric in the two directions (eq.
+   * adi:poisson transposed: A_y U^T M_x + M_y U^T A_x = G^T), so when the
+   * long bubble chains lie along y (chains > 64 positions, beyond the TMA
+   * y-solve kernel) but not along x, the plan runs Alg. 2 on the transposed
+   * equation (swap = true): ox / oy are the directions of the SOLVE (ox = the
+   * caller's y), oP / oQ its shifts (zolotarev with the intervals swapped),
+   * the factor tables, layout, workspace and stencil tables are built in
+   * that orientation, and copy-in / finalize transpose G and U (DESIGN.md
+   * §6, reading R23).  Otherwise ox = dx, oy = dy, oP = P, oQ = Q. */
+  bool swap = false;
+  DirDev ox{}, oy{};
+  std::vector<double> oP, oQ;
   Tuning tun{};                   // environment switches, read once at plan time
   long long launches = 0;
   // profiling (hpfem_plan_profile)
@@ -465,18 +478,18 @@ int alloc_workspace(hpfem_plan_t pl, Workspace& w, cudaStream_t st) {
     return e == cudaErrorMemoryAllocation ? set_err(HPFEM_ENOMEM, std::string(what) + ": out of device memory")
                                           : cuda_err(e, what);
   };
-  const size_t bytes = sizeof(double) * ((size_t)pl->hx.N * pl->lay.ld + 64);  // +slack for bulk copies
+  const size_t bytes = sizeof(double) * ((size_t)pl->ox.N * pl->lay.ld + 64);  // +slack for bulk copies
   for (double** b : {&w.Gp, &w.X1, &w.X2}) {
     if ((ce = cudaMalloc(b, bytes)) != cudaSuccess) return fail(ce, "alloc workspace");
     if ((ce = cudaMemsetAsync(*b, 0, bytes, st)) != cudaSuccess) return fail(ce, "memset workspace");
   }
   if (pl->use_tma) {
-    const size_t zb = sizeof(double) * ((size_t)pl->hx.N * 2 * pl->dy.n + 64);
+    const size_t zb = sizeof(double) * ((size_t)pl->ox.N * 2 * pl->oy.n + 64);
     if ((ce = cudaMalloc(&w.Z01, zb)) != cudaSuccess) return fail(ce, "alloc workspace");
     if ((ce = cudaMemsetAsync(w.Z01, 0, zb, st)) != cudaSuccess) return fail(ce, "memset workspace");
   }
   double* const arrays[3] = {w.Gp, w.X1, w.X2};
-  w.tma = tma_plan_create(pl->dx, pl->dy, pl->lay, arrays, pl->use_tma, pl->tun.eg_y);
+  w.tma = tma_plan_create(pl->ox, pl->oy, pl->lay, arrays, pl->use_tma, pl->tun.eg_y);
   if (pl->use_tma && !tma_supports(w.tma, 0)) return fail(cudaErrorNotSupported, "TMA tensor maps");
   if (pl->use_tma) {
     if ((ce = cudaStreamCreateWithFlags(&w.hs, cudaStreamNonBlocking)) != cudaSuccess ||
@@ -584,8 +597,33 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
         (ce = launch_load_tab(pl->dy, const_cast<int*>(pl->dy.lr), const_cast<double*>(pl->dy.lw), st)) != cudaSuccess)
       return fail_cuda(ce, "load tables");
   }
-  pl->sx = fac_stride(pl->dx);
-  pl->sy = fac_stride(pl->dy);
+  // solve orientation (see hpfem_plan_s::swap): transposed when only that
+  // makes the half-steps expressible by the TMA kernels (or when forced by
+  // HPFEM_TRANSPOSE=1 for testing), and only with the same J
+  pl->ox = pl->dx;
+  pl->oy = pl->dy;
+  pl->oP = pl->P;
+  pl->oQ = pl->Q;
+  {
+    const int tr = pl->tun.transpose;
+    const bool want = tr == 1 || (tr < 0 && !pl->tun.no_tma && !tma_shape_ok(pl->dx, pl->dy, pl->tun.eg_y) &&
+                                  tma_shape_ok(pl->dy, pl->dx, pl->tun.eg_y));
+    if (want) {
+      int Js = 0;
+      double gs = 0.0;
+      std::vector<double> sP, sQ;
+      if (zolotarev(pl->lam_y[0], pl->lam_y[1], -pl->lam_x[1], -pl->lam_x[0], tol, Js, gs, sP, sQ) == HPFEM_OK &&
+          Js == J) {
+        pl->swap = true;
+        pl->ox = pl->dy;
+        pl->oy = pl->dx;
+        pl->oP = sP;
+        pl->oQ = sQ;
+      }
+    }
+  }
+  pl->sx = fac_stride(pl->ox);
+  pl->sy = fac_stride(pl->oy);
   // shift parameter tables: x: J sets (kap=1, sig = w^2/2 - q_j); y: J sets (sig = w^2/2 + p_j) + mass
   std::vector<double> sh(4 * (size_t)(J + 1), 0.0);
   double* kx = sh.data();
@@ -594,9 +632,9 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   double* sgy = ky + (J + 1);
   for (int j = 0; j < J; ++j) {
     kx[j] = 1.0;
-    sgx[j] = hw2 - pl->Q[j];
+    sgx[j] = hw2 - pl->oQ[j];
     ky[j] = 1.0;
-    sgy[j] = hw2 + pl->P[j];
+    sgy[j] = hw2 + pl->oP[j];
   }
   ky[J] = 0.0;
   sgy[J] = 1.0;  // C = M_y for the final W_J C^{-1}
@@ -604,8 +642,8 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   {  // apply shifts of the two half-steps, as solve_core forms them (A.tau, B.tau)
     std::vector<double> tau(2 * (size_t)J + 2, 0.0);
     for (int j = 0; j < J; ++j) {
-      tau[j] = hw2 - pl->P[j];
-      tau[J + j] = hw2 + pl->Q[j];
+      tau[j] = hw2 - pl->oP[j];
+      tau[J + j] = hw2 + pl->oQ[j];
     }
     if ((ce = cudaMalloc(&pl->d_tau, sizeof(double) * tau.size())) != cudaSuccess) return fail_cuda(ce, "alloc");
     if ((ce = cudaMemcpyAsync(pl->d_tau, tau.data(), sizeof(double) * tau.size(), cudaMemcpyHostToDevice, st)) !=
@@ -623,36 +661,36 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
   if ((ce = cudaMemsetAsync(pl->fx, 0, sizeof(double) * pl->sx * J, st)) != cudaSuccess) return fail_cuda(ce, "memset");
   if ((ce = cudaMemsetAsync(pl->fy, 0, sizeof(double) * pl->sy * (J + 1), st)) != cudaSuccess)
     return fail_cuda(ce, "memset");
-  pl->use_tma = !pl->tun.no_tma && tma_shape_ok(pl->dx, pl->dy, pl->tun.eg_y);
-  pl->lay = make_layout(pl->dy, pl->use_tma ? 1 : 0);
+  pl->use_tma = !pl->tun.no_tma && tma_shape_ok(pl->ox, pl->oy, pl->tun.eg_y);
+  pl->lay = make_layout(pl->oy, pl->use_tma ? 1 : 0);
   if ((rc = alloc_workspace(pl, pl->ws, st)) != HPFEM_OK) {
     free_plan(pl);
     return rc;
   }
   if (pl->use_tma && !pl->tun.no_wtab) {  // stencil-weight tables of every ST_APPLY half-step
-    pl->wxs = tma_wtab_doubles(pl->dx, pl->dy, pl->lay, 0);
-    pl->wys = tma_wtab_doubles(pl->dx, pl->dy, pl->lay, 1);
+    pl->wxs = tma_wtab_doubles(pl->ox, pl->oy, pl->lay, 0);
+    pl->wys = tma_wtab_doubles(pl->ox, pl->oy, pl->lay, 1);
     if ((ce = cudaMalloc(&pl->wx, sizeof(double) * pl->wxs * J)) != cudaSuccess) return fail_cuda(ce, "alloc wx");
     if ((ce = cudaMalloc(&pl->wy, sizeof(double) * pl->wys * J)) != cudaSuccess) return fail_cuda(ce, "alloc wy");
     if ((ce = cudaMemsetAsync(pl->wx, 0, sizeof(double) * pl->wxs * J, st)) != cudaSuccess) return fail_cuda(ce, "memset");
     if ((ce = cudaMemsetAsync(pl->wy, 0, sizeof(double) * pl->wys * J, st)) != cudaSuccess) return fail_cuda(ce, "memset");
   }
   const double* dsh = pl->d_shift;
-  if ((ce = launch_factor(pl->dx, dsh, dsh + (J + 1), J, pl->fx, pl->sx, pl->d_err, st)) != cudaSuccess)
+  if ((ce = launch_factor(pl->ox, dsh, dsh + (J + 1), J, pl->fx, pl->sx, pl->d_err, st)) != cudaSuccess)
     return fail_cuda(ce, "factor x");
-  if ((ce = launch_factor(pl->dy, dsh + 2 * (J + 1), dsh + 3 * (J + 1), J + 1, pl->fy, pl->sy, pl->d_err + 4, st)) !=
+  if ((ce = launch_factor(pl->oy, dsh + 2 * (J + 1), dsh + 3 * (J + 1), J + 1, pl->fy, pl->sy, pl->d_err + 4, st)) !=
       cudaSuccess)
     return fail_cuda(ce, "factor y");
   if (pl->wx) {
     for (int j = 0; j < J; ++j) {
       // half-step B of iteration j: y-apply (A_y + q_j M_y) Corr_y(fy[j]) along the x-solve lines
-      const FacView fyj = fac_view(pl->dy, pl->fy + pl->sy * j, 1.0, hw2 + pl->P[j]);
-      if ((ce = tma_build_wtab(pl->dx, pl->dy, pl->lay, 0, 1.0, hw2 + pl->Q[j], fyj.vL, fyj.vR,
+      const FacView fyj = fac_view(pl->oy, pl->fy + pl->sy * j, 1.0, hw2 + pl->oP[j]);
+      if ((ce = tma_build_wtab(pl->ox, pl->oy, pl->lay, 0, 1.0, hw2 + pl->oQ[j], fyj.vL, fyj.vR,
                                pl->wx + pl->wxs * j, st)) != cudaSuccess)
         return fail_cuda(ce, "stencil tables");
       if (j == 0) continue;  // half-step A of iteration 0 has no apply (W_0 = 0)
-      const FacView fxp = fac_view(pl->dx, pl->fx + pl->sx * (j - 1), 1.0, hw2 - pl->Q[j - 1]);
-      if ((ce = tma_build_wtab(pl->dx, pl->dy, pl->lay, 1, 1.0, hw2 - pl->P[j], fxp.vL, fxp.vR,
+      const FacView fxp = fac_view(pl->ox, pl->fx + pl->sx * (j - 1), 1.0, hw2 - pl->oQ[j - 1]);
+      if ((ce = tma_build_wtab(pl->ox, pl->oy, pl->lay, 1, 1.0, hw2 - pl->oP[j], fxp.vL, fxp.vR,
                                pl->wy + pl->wys * j, st)) != cudaSuccess)
         return fail_cuda(ce, "stencil tables");
     }
@@ -678,9 +716,9 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
 FacView fview(hpfem_plan_t pl, int dir, int set) {
   const int J = pl->J;
   const double hw2 = 0.5 * pl->omega * pl->omega;
-  if (dir == 0) return fac_view(pl->dx, pl->fx + pl->sx * set, 1.0, hw2 - pl->Q[set]);
-  if (set == J) return fac_view(pl->dy, pl->fy + pl->sy * set, 0.0, 1.0);
-  return fac_view(pl->dy, pl->fy + pl->sy * set, 1.0, hw2 + pl->P[set]);
+  if (dir == 0) return fac_view(pl->ox, pl->fx + pl->sx * set, 1.0, hw2 - pl->oQ[set]);
+  if (set == J) return fac_view(pl->oy, pl->fy + pl->sy * set, 0.0, 1.0);
+  return fac_view(pl->oy, pl->fy + pl->sy * set, 1.0, hw2 + pl->oP[set]);
 }
 
 bool overlap(const void* a, const void* b, size_t bytes) {
@@ -796,6 +834,15 @@ int hpfem_plan_dims(hpfem_plan_t pl, int* n_x, int* p_x, int* n_y, int* p_y) {
   return HPFEM_OK;
 }
 
+static bool small_path(hpfem_plan_t pl);
+
+int hpfem_plan_path(hpfem_plan_t pl, int* path, int* transposed) {
+  if (!pl) return set_err(HPFEM_EINVAL, "null plan");
+  if (path) *path = small_path(pl) ? 0 : (pl->use_tma ? 1 : 2);
+  if (transposed) *transposed = pl->swap ? 1 : 0;
+  return HPFEM_OK;
+}
+
 int hpfem_plan_shifts(hpfem_plan_t pl, double* p, double* q) {
   if (!pl) return set_err(HPFEM_EINVAL, "null plan");
   if (p) std::memcpy(p, pl->P.data(), sizeof(double) * pl->J);
@@ -815,7 +862,11 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
   int rc;
   {
     const int e0 = prof_mark(pl, st);
-    if ((rc = count_launch(pl, launch_copyin(pl->dx, pl->dy, pl->lay, F, w.Gp, st), "copy-in"))) return rc;
+    if (pl->swap) {  // G^T into the scratch iterate X2 (dead until half-step B writes it)
+      if ((rc = count_launch(pl, launch_transpose(F, pl->hx.N, pl->hy.N, w.X2, st), "transpose"))) return rc;
+      F = w.X2;
+    }
+    if ((rc = count_launch(pl, launch_copyin(pl->ox, pl->oy, pl->lay, F, w.Gp, st), "copy-in"))) return rc;
     prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);  // layout change, not algorithmic
   }
   auto base = [&](int dir) {
@@ -823,8 +874,8 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
     P.dir = dir;
     P.ld = pl->lay.ld;
     P.lay = pl->lay;
-    P.s = dir == 0 ? pl->dx : pl->dy;
-    P.o = dir == 0 ? pl->dy : pl->dx;
+    P.s = dir == 0 ? pl->ox : pl->oy;
+    P.o = dir == 0 ? pl->oy : pl->ox;
     P.lp_begin = 0;
     P.lp_count = P.o.N;
     return P;
@@ -845,7 +896,7 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
       A.mode = ST_APPLY;
       A.Xp = w.X2;
       A.kap_a = 1.0;
-      A.tau = hw2 - pl->P[j];
+      A.tau = hw2 - pl->oP[j];
       A.cvL = prev.vL;
       A.cvR = prev.vR;
       if (pl->wy) A.wtab = pl->wy + pl->wys * j;
@@ -864,7 +915,7 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
     B.Xp = w.X1;
     B.z01p = w.Z01;
     B.kap_a = 1.0;
-    B.tau = hw2 + pl->Q[j];
+    B.tau = hw2 + pl->oQ[j];
     B.cvL = A.f.vL;
     B.cvR = A.f.vR;
     if (pl->wx) B.wtab = pl->wx + pl->wxs * j;
@@ -888,7 +939,10 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
   Fin.cvR = last.vR;
   if ((rc = run_step(pl, w, Fin, st, true, -1, 2))) return rc;
   const int e0 = prof_mark(pl, st);
-  rc = count_launch(pl, launch_finalize(pl->dx, pl->dy, pl->lay, Fin.f.vL, Fin.f.vR, w.X1, U, st), "finalize");
+  // (swap: U^T into the dead iterate X2, then transposed into U)
+  rc = count_launch(pl, launch_finalize(pl->ox, pl->oy, pl->lay, Fin.f.vL, Fin.f.vR, w.X1, pl->swap ? w.X2 : U, st),
+                    "finalize");
+  if (!rc && pl->swap) rc = count_launch(pl, launch_transpose(w.X2, pl->ox.N, pl->oy.N, U, st), "transpose");
   prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);
   return rc;
 }
@@ -942,7 +996,7 @@ static int solve_graph(hpfem_plan_t pl, const Workspace& w, const double* F, dou
  * profiling, so that the per-kind profile stays the multi-kernel path's) */
 static bool small_path(hpfem_plan_t pl) {
   if (pl->tun.no_small) return false;
-  return pl->ev.empty() && small_smem_bytes(pl->dx, pl->dy) <= SMALL_SMEM_MAX;
+  return !pl->swap && pl->ev.empty() && small_smem_bytes(pl->dx, pl->dy) <= SMALL_SMEM_MAX;
 }
 
 static int solve_small(hpfem_plan_t pl, int batch, const double* F, double* U, int iters, cudaStream_t st);

@@ -270,38 +270,70 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
 #pragma unroll
       for (int k = 0; k < 5; ++k) st.w[k] = 0.0;
     }
-    double ys[CL];
+    // chain positions [0, CR) stay in registers; longer chains (CL = 128:
+    // the long direction of a transposed solve) park the down-
+    // sweep values of positions >= CR at their final addresses in `out` (a
+    // coalesced 256-byte row per warp, read back by the same thread in the up
+    // sweep: an L2 round trip) and overwrite them with z.  The spilled stages
+    // run as a rolled loop (the fully unrolled 128-position body overflowed
+    // the instruction cache: ncu no_instruction stalls 12 per issue).
+    constexpr int CR = CL > 64 ? 64 : CL;
+    double ys[CR];
+    double* __restrict__ outc = P.out + P.lay.hb + (size_t)(valid ? ey : 0) * Q + ky;
+    auto orow = [&](int c) { return (size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld; };
     double yv = 0.0;
+    // one ring stage: wait, stencil of its KR rows, release, return r values
+    auto stage_rhs = [&](int sg, double* rv) {
+      const int slot = cslot;
+      mbar_wait(&full[slot], cround & 1);
+      if (wtab && KR * sg + KR >= mS) {  // first stage of the tile: the weights have landed
 #pragma unroll
-    for (int sg = CL / KR - 1; sg >= 0; --sg) {
+        for (int k = 0; k < 5; ++k) st.w[k] = valid ? wb[(eo * 5 + k) * Q + ky] : 0.0;
+      }
+      const unsigned char* stg = ring + (size_t)slot * A.stage_bytes;
+#pragma unroll
+      for (int kk = 0; kk < KR; ++kk) {
+        const double* Gs = reinterpret_cast<const double*>(stg) + kk * BW;
+        const double* Ws = reinterpret_cast<const double*>(stg + A.off_w) + kk * BW;
+        const double* Hs = reinterpret_cast<const double*>(stg + A.off_h) + kk * A.hw;
+        double r = 0.0;
+        if (MODE != ST_CORR) r = Gs[o0];
+        if (MODE != ST_NONE)
+          r += st.w[0] * Ws[o0] + st.w[1] * Ws[o1] + st.w[2] * Ws[o2] + st.w[3] * Hs[o3] + st.w[4] * Hs[o4];
+        rv[kk] = r;
+      }
+      __syncwarp();
+      if (lane == 0 && release_is_last(cnt, slot))
+        x_issue<MODE>(A, gs + NST, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
+      ++gs;
+      if (++cslot == NST) {
+        cslot = 0;
+        ++cround;
+      }
+    };
+    if (CL > CR) {  // spilled stages (positions >= CR), rolled
+#pragma unroll 1
+      for (int sg = CL / KR - 1; sg >= CR / KR; --sg) {
+        if (KR * sg < mS) {
+          double rv[KR];
+          stage_rhs(sg, rv);
+#pragma unroll
+          for (int kk = KR - 1; kk >= 0; --kk) {
+            const int c = KR * sg + kk;
+            if (c < m) {
+              const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c);  // (il, hd)
+              yv = fma(-f.y, yv, f.x * rv[kk]);
+              if (valid) outc[orow(c)] = yv;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int sg = CR / KR - 1; sg >= 0; --sg) {
       if (KR * sg < mS) {
-        const int slot = cslot;
-        mbar_wait(&full[slot], cround & 1);
-        if (wtab && KR * sg + KR >= mS) {  // first stage of the tile: the weights have landed
-#pragma unroll
-          for (int k = 0; k < 5; ++k) st.w[k] = valid ? wb[(eo * 5 + k) * Q + ky] : 0.0;
-        }
-        const unsigned char* stg = ring + (size_t)slot * A.stage_bytes;
         double rv[KR];
-#pragma unroll
-        for (int kk = 0; kk < KR; ++kk) {
-          const double* Gs = reinterpret_cast<const double*>(stg) + kk * BW;
-          const double* Ws = reinterpret_cast<const double*>(stg + A.off_w) + kk * BW;
-          const double* Hs = reinterpret_cast<const double*>(stg + A.off_h) + kk * A.hw;
-          double r = 0.0;
-          if (MODE != ST_CORR) r = Gs[o0];
-          if (MODE != ST_NONE)
-            r += st.w[0] * Ws[o0] + st.w[1] * Ws[o1] + st.w[2] * Ws[o2] + st.w[3] * Hs[o3] + st.w[4] * Hs[o4];
-          rv[kk] = r;
-        }
-        __syncwarp();
-        if (lane == 0 && release_is_last(cnt, slot))
-          x_issue<MODE>(A, gs + NST, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
-        ++gs;
-        if (++cslot == NST) {
-          cslot = 0;
-          ++cround;
-        }
+        stage_rhs(sg, rv);
 #pragma unroll
         for (int kk = KR - 1; kk >= 0; --kk) {
           const int c = KR * sg + kk;
@@ -314,11 +346,11 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
       }
     }
     if (valid) {
-      double* __restrict__ out = P.out + P.lay.hb + (size_t)ey * Q + ky;
+      double* __restrict__ out = outc;
       double z = 0.0;
       // factor pairs loaded KR at a time ahead of the stores (as in the y-solve)
 #pragma unroll
-      for (int c0 = 0; c0 < CL; c0 += KR) {
+      for (int c0 = 0; c0 < CR; c0 += KR) {
         if (c0 < m) {
           double2 fz[KR];
 #pragma unroll
@@ -328,7 +360,35 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
             const int c = c0 + u;
             if (c < m) {
               z = fma(-fz[u].x, z, fz[u].y * ys[c]);
-              out[(size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld] = z;
+              out[orow(c)] = z;
+            }
+          }
+        }
+      }
+      if (CL > CR) {  // spilled positions, rolled; y loaded one batch ahead
+        double yn[KR];
+#pragma unroll
+        for (int u = 0; u < KR; ++u) yn[u] = CR + u < m ? out[orow(CR + u)] : 0.0;
+#pragma unroll 1
+        for (int c0 = CR; c0 < m; c0 += KR) {
+          double yc[KR];
+          double2 fz[KR];
+#pragma unroll
+          for (int u = 0; u < KR; ++u) {
+            yc[u] = yn[u];
+            fz[u] = *reinterpret_cast<const double2*>(fb + 4 * (c0 + u) + 2);  // (hu, il)
+          }
+#pragma unroll
+          for (int u = 0; u < KR; ++u) {
+            const int c = c0 + KR + u;
+            yn[u] = c < m ? out[orow(c)] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < KR; ++u) {
+            const int c = c0 + u;
+            if (c < m) {
+              z = fma(-fz[u].x, z, fz[u].y * yc[u]);
+              out[orow(c)] = z;
             }
           }
         }
@@ -734,7 +794,7 @@ bool tma_shape_ok(const DirDev& x, const DirDev& y, int eg_y) {
   const int Q = even_up(y.p - 1);
   int EG, R;
   y_tile_shape(x, y, eg_y, EG, R);
-  return x.nb > 0 && y.nb > 0 && x.N >= 2 && Q <= 256 && Q >= KBOX && chain_len(x.p, 0) <= 64 &&
+  return x.nb > 0 && y.nb > 0 && x.N >= 2 && Q <= 256 && Q >= KBOX && chain_len(x.p, 0) <= 128 &&
          chain_len(y.p, 0) <= 64 && R >= 16 / EG;
 }
 
@@ -838,7 +898,8 @@ static cudaError_t dispatch_x(int cl, const TmaStepArgs& A, const CUtensorMap* g
   if (cl <= 8) return launch_x<8, MODE>(A, g, w, grid, smem, st);
   if (cl <= 16) return launch_x<16, MODE>(A, g, w, grid, smem, st);
   if (cl <= 32) return launch_x<32, MODE>(A, g, w, grid, smem, st);
-  return launch_x<64, MODE>(A, g, w, grid, smem, st);
+  if (cl <= 64) return launch_x<64, MODE>(A, g, w, grid, smem, st);
+  return launch_x<128, MODE>(A, g, w, grid, smem, st);
 }
 
 template <int MODE, int EGT>

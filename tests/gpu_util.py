@@ -104,3 +104,27 @@ def golden_floor(key):
     import os
 
     return json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_floor.json")))[key]
+
+
+def swapped_problem(xs, px, ys, py, bc, robin=None):
+    """The transposed problem (x <-> y) of the same equation: arguments for
+    the oracle when the plan solves A_y U^T M_x + M_y U^T A_x = G^T (reading
+    R23, hpfem_plan_path reports it)."""
+    bx, by = oracle.split_bc(bc)
+    rob = None if robin is None else [robin[2], robin[3], robin[0], robin[1]]
+    return ys, py, xs, px, oracle.bc2d(by, bx), rob
+
+
+def oracle_reference(plan, xs, px, ys, py, om, bc, tol, G, iters=-1, floor=True):
+    """(floor dict or None, Uref) from the oracle running Alg. 2 in the same
+    orientation as the plan (the transposed equation when the plan is
+    transposed; U returned in the caller's layout either way)."""
+    tr = plan.path()["transposed"]
+    if tr:
+        xs, px, ys, py, bc, _ = swapped_problem(xs, px, ys, py, bc)
+        G = np.ascontiguousarray(np.asarray(G).T)
+    if floor:
+        fl, U = oracle.rounding_floor(xs, px, ys, py, om, bc, tol, G, iters)
+    else:
+        fl, (U, _) = None, oracle.adi_solve(xs, px, ys, py, om, bc, tol, G, iters)
+    return fl, (np.ascontiguousarray(U.T) if tr else U)
