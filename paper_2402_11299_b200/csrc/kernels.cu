@@ -758,6 +758,71 @@ static cudaError_t launch_hats_dir(const StepParams& P, cudaStream_t st) {
 #endif
 constexpr int EGH = HPFEM_EGH;  // y-elements per hat-row CTA
 
+struct Aff {  // y = a + b * y_in
+  double a, b;
+};
+
+__device__ __forceinline__ Aff aff_after(const Aff& f, const Aff& g) {  // f o g
+  return Aff{fma(f.b, g.a, f.a), f.b * g.b};
+}
+
+/* Warp-cooperative in-place solve of one bubble chain (m <= 64) held in
+ * shared memory, v[c * vs], with the chain-major factors f ([4c] il,
+ * [4c+1] hd = g il, [4c+2] hu = g_prev il): lane L owns positions 2L, 2L+1;
+ * each first-order recurrence (y_c = il_c v_c - hd_c y_{c+1} down, z_c =
+ * il_c y_c - hu_c z_{c-1} up) is composed into per-lane affine maps, scanned
+ * over the warp with shuffles and swept locally: ~14 dependent steps
+ * instead of 2m (the scan form of the hat Schur kernels). */
+__device__ __forceinline__ void chain_solve_warp(const double* f, double* v, int vs, int m) {
+  const int lane = threadIdx.x & 31;
+  const int c0 = 2 * lane;
+  double r[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) r[u] = c0 + u < m ? v[(c0 + u) * vs] : 0.0;
+  Aff fm{0.0, 1.0};
+#pragma unroll
+  for (int u = 1; u >= 0; --u) {
+    const int c = c0 + u;
+    if (c < m) fm = Aff{fma(-f[4 * c + 1], fm.a, f[4 * c] * r[u]), -f[4 * c + 1] * fm.b};
+  }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Aff g{__shfl_down_sync(0xffffffffu, fm.a, d), __shfl_down_sync(0xffffffffu, fm.b, d)};
+    if (lane + d < 32) fm = aff_after(fm, g);
+  }
+  double yv = __shfl_down_sync(0xffffffffu, fm.a, 1);
+  if (lane == 31) yv = 0.0;
+#pragma unroll
+  for (int u = 1; u >= 0; --u) {
+    const int c = c0 + u;
+    if (c < m) {
+      yv = fma(-f[4 * c + 1], yv, f[4 * c] * r[u]);
+      r[u] = yv;
+    }
+  }
+  fm = Aff{0.0, 1.0};
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int c = c0 + u;
+    if (c < m) fm = Aff{fma(-f[4 * c + 2], fm.a, f[4 * c] * r[u]), -f[4 * c + 2] * fm.b};
+  }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Aff g{__shfl_up_sync(0xffffffffu, fm.a, d), __shfl_up_sync(0xffffffffu, fm.b, d)};
+    if (lane >= d) fm = aff_after(fm, g);
+  }
+  double zv = __shfl_up_sync(0xffffffffu, fm.a, 1);
+  if (lane == 0) zv = 0.0;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int c = c0 + u;
+    if (c < m) {
+      zv = fma(-f[4 * c + 2], zv, f[4 * c] * r[u]);
+      v[c * vs] = zv;
+    }
+  }
+}
+
 /* In-place solve of one bubble chain held in shared memory, v[c * vs],
  * c < m, with the chain-major factors f ([4c] il, [4c+1] g il, [4c+2]
  * g_prev il): y_c = il_c v_c - hd_c y_{c+1} downwards, then z_c = il_c y_c -
@@ -865,6 +930,8 @@ __global__ void __launch_bounds__(128) k_hatrows_y(StepParams P) {
   }
   __syncthreads();
   // chains: thread (eo, pi); down sweep y, up sweep z, in place
+  // (a warp-scan variant, chain_solve_warp, measured 54 -> 66 us per launch
+  // at config 5: the chains are not this kernel's limiter)
   if (threadIdx.x < 2 * ne) {
     const int eo = threadIdx.x >> 1, pi = threadIdx.x & 1;
     const int m = chain_len(y.p, pi);
@@ -964,35 +1031,70 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
   }
   mbar_wait(&bar, 0);
   __syncthreads();
-  if (threadIdx.x < nl) {
-    const int l = l0 + threadIdx.x;
-    Stencil st;
-    stencil_build(y, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
-    int off[7];
+  // right-hand sides and the chain solves split over the 8 warps: thread
+  // (column j, warp w) owns chain positions [w BP, w BP + BP) of column j;
+  // the block maps of the two recurrences are folded through shared memory
+  // (the x chains run to 128 positions on the transposed path)
+  {
+    const int j = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const bool act = j < nl;
+    double* fa = fac + cfs;  // [8][32] block maps (after the factors)
+    double* fbm = fa + 8 * 32;
+    const int BP = (m + 7) >> 3, ca = w * BP, cb = min(m, ca + BP);
+    if (act) {
+      const int l = l0 + j;
+      Stencil st;
+      stencil_build(y, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+      int off[7];
 #pragma unroll
-    for (int q = 0; q < 7; ++q) {
-      const int d = st.idx[q];
-      if (d < 0) {
-        off[q] = 0;
-        st.w[q] = 0.0;
-      } else if (d < y.nh) {
-        off[q] = TC + (d - hlo);
-      } else {
-        const int b = d - y.nh, k = b / y.n, e = b - k * y.n;
-        off[q] = TC + HREG + 2 * (e - elo) + k;
+      for (int q = 0; q < 7; ++q) {
+        const int d = st.idx[q];
+        if (d < 0) {
+          off[q] = 0;
+          st.w[q] = 0.0;
+        } else if (d < y.nh) {
+          off[q] = TC + (d - hlo);
+        } else {
+          const int b = d - y.nh, k = b / y.n, e = b - k * y.n;
+          off[q] = TC + HREG + 2 * (e - elo) + k;
+        }
+      }
+      const double aG = P.alphaG;
+      // right-hand sides in place (each thread reads its stencil columns and
+      // overwrites only its own G slot)
+      for (int c = ca; c < cb; ++c) {
+        const double* R = rows + (size_t)c * RW;
+        double r = aG != 0.0 ? aG * R[j] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) r += st.w[q] * R[off[q]];
+        rows[(size_t)c * RW + j] = r;
       }
     }
-    const double aG = P.alphaG;
-    // right-hand sides in place (each thread reads its stencil columns and
-    // overwrites only its own G column), then the chain solve
-    for (int c = 0; c < m; ++c) {
-      const double* R = rows + (size_t)c * RW;
-      double r = aG != 0.0 ? aG * R[threadIdx.x] : 0.0;
-#pragma unroll
-      for (int q = 0; q < 7; ++q) r += st.w[q] * R[off[q]];
-      rows[(size_t)c * RW + threadIdx.x] = r;
+    Aff f1{0.0, 1.0};
+    for (int c = cb - 1; c >= ca; --c)
+      f1 = Aff{fma(-fac[4 * c + 1], f1.a, fac[4 * c] * rows[(size_t)c * RW + j]), -fac[4 * c + 1] * f1.b};
+    fa[w * 32 + j] = f1.a;
+    fbm[w * 32 + j] = f1.b;
+    __syncthreads();
+    double yv = 0.0;
+    for (int u = 7; u > w; --u) yv = fma(fbm[u * 32 + j], yv, fa[u * 32 + j]);
+    for (int c = cb - 1; c >= ca; --c) {
+      yv = fma(-fac[4 * c + 1], yv, fac[4 * c] * rows[(size_t)c * RW + j]);
+      rows[(size_t)c * RW + j] = yv;
     }
-    chain_solve_smem(fac, rows + threadIdx.x, RW, m);
+    f1 = Aff{0.0, 1.0};
+    for (int c = ca; c < cb; ++c)
+      f1 = Aff{fma(-fac[4 * c + 2], f1.a, fac[4 * c] * rows[(size_t)c * RW + j]), -fac[4 * c + 2] * f1.b};
+    __syncthreads();
+    fa[w * 32 + j] = f1.a;
+    fbm[w * 32 + j] = f1.b;
+    __syncthreads();
+    double zv = 0.0;
+    for (int u = 0; u < w; ++u) zv = fma(fbm[u * 32 + j], zv, fa[u * 32 + j]);
+    for (int c = ca; c < cb; ++c) {
+      zv = fma(-fac[4 * c + 2], zv, fac[4 * c] * rows[(size_t)c * RW + j]);
+      rows[(size_t)c * RW + j] = zv;
+    }
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < m * TC; idx += blockDim.x) {
@@ -1013,7 +1115,7 @@ cudaError_t launch_hat_lines(const StepParams& P, cudaStream_t st) {
     k_hatrows_y<<<grid, 128, smem, st>>>(P);
   } else {
     const int m = chain_len(P.s.p, 0);
-    const size_t smem = sizeof(double) * ((size_t)m * (TC + HREG + 2 * (TC + 2)) + P.f.cfs);
+    const size_t smem = sizeof(double) * ((size_t)m * (TC + HREG + 2 * (TC + 2)) + P.f.cfs + 2 * 8 * 32);
     cudaError_t e = smem_optin((const void*)k_hatcols_x, smem);
     if (e != cudaSuccess) return e;
     dim3 grid(P.s.n * 2, (P.o.nh + TC - 1) / TC);
@@ -1037,13 +1139,6 @@ cudaError_t launch_hat_lines(const StepParams& P, cudaStream_t st) {
 /* differs from the sequential sweep (rounding-level, checked against   */
 /* the oracle's rounding floor in tests/test_gpu_parity.py).            */
 /* ------------------------------------------------------------------ */
-struct Aff {  // y = a + b * y_in
-  double a, b;
-};
-
-__device__ __forceinline__ Aff aff_after(const Aff& f, const Aff& g) {  // f o g
-  return Aff{fma(f.b, g.a, f.a), f.b * g.b};
-}
 
 /* per-hat tables of a hat Schur CTA: il, hd, hu, and the couplings
  * B(h, W_0 / W_1) of the left / right element (0 where absent) */
