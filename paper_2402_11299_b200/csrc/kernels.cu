@@ -766,63 +766,6 @@ __device__ __forceinline__ Aff aff_after(const Aff& f, const Aff& g) {  // f o g
   return Aff{fma(f.b, g.a, f.a), f.b * g.b};
 }
 
-/* Warp-cooperative in-place solve of one bubble chain (m <= 64) held in
- * shared memory, v[c * vs], with the chain-major factors f ([4c] il,
- * [4c+1] hd = g il, [4c+2] hu = g_prev il): lane L owns positions 2L, 2L+1;
- * each first-order recurrence (y_c = il_c v_c - hd_c y_{c+1} down, z_c =
- * il_c y_c - hu_c z_{c-1} up) is composed into per-lane affine maps, scanned
- * over the warp with shuffles and swept locally: ~14 dependent steps
- * instead of 2m (the scan form of the hat Schur kernels). */
-__device__ __forceinline__ void chain_solve_warp(const double* f, double* v, int vs, int m) {
-  const int lane = threadIdx.x & 31;
-  const int c0 = 2 * lane;
-  double r[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) r[u] = c0 + u < m ? v[(c0 + u) * vs] : 0.0;
-  Aff fm{0.0, 1.0};
-#pragma unroll
-  for (int u = 1; u >= 0; --u) {
-    const int c = c0 + u;
-    if (c < m) fm = Aff{fma(-f[4 * c + 1], fm.a, f[4 * c] * r[u]), -f[4 * c + 1] * fm.b};
-  }
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const Aff g{__shfl_down_sync(0xffffffffu, fm.a, d), __shfl_down_sync(0xffffffffu, fm.b, d)};
-    if (lane + d < 32) fm = aff_after(fm, g);
-  }
-  double yv = __shfl_down_sync(0xffffffffu, fm.a, 1);
-  if (lane == 31) yv = 0.0;
-#pragma unroll
-  for (int u = 1; u >= 0; --u) {
-    const int c = c0 + u;
-    if (c < m) {
-      yv = fma(-f[4 * c + 1], yv, f[4 * c] * r[u]);
-      r[u] = yv;
-    }
-  }
-  fm = Aff{0.0, 1.0};
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int c = c0 + u;
-    if (c < m) fm = Aff{fma(-f[4 * c + 2], fm.a, f[4 * c] * r[u]), -f[4 * c + 2] * fm.b};
-  }
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const Aff g{__shfl_up_sync(0xffffffffu, fm.a, d), __shfl_up_sync(0xffffffffu, fm.b, d)};
-    if (lane >= d) fm = aff_after(fm, g);
-  }
-  double zv = __shfl_up_sync(0xffffffffu, fm.a, 1);
-  if (lane == 0) zv = 0.0;
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int c = c0 + u;
-    if (c < m) {
-      zv = fma(-f[4 * c + 2], zv, f[4 * c] * r[u]);
-      v[c * vs] = zv;
-    }
-  }
-}
-
 /* In-place solve of one bubble chain held in shared memory, v[c * vs],
  * c < m, with the chain-major factors f ([4c] il, [4c+1] g il, [4c+2]
  * g_prev il): y_c = il_c v_c - hd_c y_{c+1} downwards, then z_c = il_c y_c -
@@ -930,7 +873,7 @@ __global__ void __launch_bounds__(128) k_hatrows_y(StepParams P) {
   }
   __syncthreads();
   // chains: thread (eo, pi); down sweep y, up sweep z, in place
-  // (a warp-scan variant, chain_solve_warp, measured 54 -> 66 us per launch
+  // (a warp-scan variant of the chain solve measured 54 -> 66 us per launch
   // at config 5: the chains are not this kernel's limiter)
   if (threadIdx.x < 2 * ne) {
     const int eo = threadIdx.x >> 1, pi = threadIdx.x & 1;
