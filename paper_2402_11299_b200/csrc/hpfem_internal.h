@@ -129,7 +129,6 @@ struct Tuning {
   int nst[2];         // HPFEM_NST_X / _Y (4): TMA ring depth
   int eg_y;           // HPFEM_EG_Y (0 = automatic): y-solve tile width
   int fake_stencil;   // HPFEM_FAKE_STENCIL (0): experiment only
-  int persist;        // HPFEM_PERSIST (1): persistent one-launch solve for L2-resident problems
   int hats_seq;       // HPFEM_HATS_SEQ (0): the sequential one-thread-per-line hat Schur kernel (experiment / A-B)
   int transpose;      // HPFEM_TRANSPOSE (-1 auto, 0 never, 1 always): solve the transposed equation (R23)
 };

@@ -75,7 +75,6 @@ Tuning read_tuning() {
   t.nst[1] = env_int("HPFEM_NST_Y", 4);
   t.eg_y = env_int("HPFEM_EG_Y", 0);
   t.fake_stencil = env_int("HPFEM_FAKE_STENCIL", 0);
-  t.persist = env_int("HPFEM_PERSIST", 1);
   t.hats_seq = env_int("HPFEM_HATS_SEQ", 0);
   t.transpose = env_int("HPFEM_TRANSPOSE", -1);
   return t;
@@ -856,19 +855,17 @@ int hpfem_plan_launches(hpfem_plan_t pl, long long* launches) {
   return HPFEM_OK;
 }
 
-/* Algorithm 2 on one workspace (validated arguments, iters >= 1) */
-static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, double* U, int iters, cudaStream_t st) {
+/* The 2 iters + 1 line-solve passes of Algorithm 2 on one workspace, in
+ * order (run_step executes one). */
+struct StepRec {
+  StepParams P;
+  bool fin;        // the final W_J C^{-1} pass (profile kind 2)
+  int ia_g, ia_w;  // G / Xp among {Gp, X1, X2} (TMA tensor maps)
+};
+
+static void build_steps(hpfem_plan_t pl, const Workspace& w, int iters, std::vector<StepRec>& out) {
   const double hw2 = 0.5 * pl->omega * pl->omega;
-  int rc;
-  {
-    const int e0 = prof_mark(pl, st);
-    if (pl->swap) {  // G^T into the scratch iterate X2 (dead until half-step B writes it)
-      if ((rc = count_launch(pl, launch_transpose(F, pl->hx.N, pl->hy.N, w.X2, st), "transpose"))) return rc;
-      F = w.X2;
-    }
-    if ((rc = count_launch(pl, launch_copyin(pl->ox, pl->oy, pl->lay, F, w.Gp, st), "copy-in"))) return rc;
-    prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);  // layout change, not algorithmic
-  }
+  out.clear();
   auto base = [&](int dir) {
     StepParams P{};
     P.dir = dir;
@@ -878,9 +875,9 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
     P.o = dir == 0 ? pl->oy : pl->ox;
     P.lp_begin = 0;
     P.lp_count = P.o.N;
+    P.tun = pl->tun;
     return P;
   };
-  NvtxRange solve_range("hpfem_solve");
   for (int j = 0; j < iters; ++j) {
     // half-step A: W_{j-1/2} = (G - (A_x - p_j M_x) W_{j-1}) (A_y + p_j M_y)^{-1}
     StepParams A = base(1);
@@ -901,10 +898,7 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
       A.cvR = prev.vR;
       if (pl->wy) A.wtab = pl->wy + pl->wys * j;
     }
-    {
-      NvtxRange r("ADI half-step A (y-solves)");
-      if ((rc = run_step(pl, w, A, st, false, 0, j == 0 ? -1 : 2))) return rc;
-    }
+    out.push_back({A, false, 0, j == 0 ? -1 : 2});
     // half-step B: W_j = (A_x - q_j M_x)^{-1} (G - W_{j-1/2} (A_y + q_j M_y))
     StepParams B = base(0);
     B.G = w.Gp;
@@ -919,13 +913,9 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
     B.cvL = A.f.vL;
     B.cvR = A.f.vR;
     if (pl->wx) B.wtab = pl->wx + pl->wxs * j;
-    {
-      NvtxRange r("ADI half-step B (x-solves)");
-      if ((rc = run_step(pl, w, B, st, false, 0, 1))) return rc;
-    }
+    out.push_back({B, false, 0, 1});
   }
-  // RETURN W_J C^{-1}: y-solves with the mass factor, then materialise U
-  NvtxRange rf("final W_J C^-1");
+  // RETURN W_J C^{-1}: y-solves with the mass factor (then finalize materialises U)
   StepParams Fin = base(1);
   Fin.G = nullptr;
   Fin.alphaG = 0.0;
@@ -937,7 +927,29 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
   const FacView last = fview(pl, 0, iters - 1);
   Fin.cvL = last.vL;
   Fin.cvR = last.vR;
-  if ((rc = run_step(pl, w, Fin, st, true, -1, 2))) return rc;
+  out.push_back({Fin, true, -1, 2});
+}
+
+/* Algorithm 2 on one workspace (validated arguments, iters >= 1) */
+static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, double* U, int iters, cudaStream_t st) {
+  int rc;
+  {
+    const int e0 = prof_mark(pl, st);
+    if (pl->swap) {  // G^T into the scratch iterate X2 (dead until half-step B writes it)
+      if ((rc = count_launch(pl, launch_transpose(F, pl->hx.N, pl->hy.N, w.X2, st), "transpose"))) return rc;
+      F = w.X2;
+    }
+    if ((rc = count_launch(pl, launch_copyin(pl->ox, pl->oy, pl->lay, F, w.Gp, st), "copy-in"))) return rc;
+    prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);  // layout change, not algorithmic
+  }
+  std::vector<StepRec> steps;
+  build_steps(pl, w, iters, steps);
+  NvtxRange solve_range("hpfem_solve");
+  for (const StepRec& r : steps) {
+    NvtxRange nr(r.fin ? "final W_J C^-1" : (r.P.dir == 1 ? "ADI half-step A (y-solves)" : "ADI half-step B (x-solves)"));
+    if ((rc = run_step(pl, w, r.P, st, r.fin, r.ia_g, r.ia_w))) return rc;
+  }
+  const StepParams& Fin = steps.back().P;
   const int e0 = prof_mark(pl, st);
   // (swap: U^T into the dead iterate X2, then transposed into U)
   rc = count_launch(pl, launch_finalize(pl->ox, pl->oy, pl->lay, Fin.f.vL, Fin.f.vR, w.X1, pl->swap ? w.X2 : U, st),
@@ -946,7 +958,6 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
   prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);
   return rc;
 }
-
 
 /* solve_core replayed from a CUDA graph: the whole solve (6J + 3 kernels and
  * the side-stream fork/joins) is captured once per (workspace, F, U, iters)

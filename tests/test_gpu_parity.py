@@ -74,7 +74,8 @@ def kernel_path(request, monkeypatch):
     (HPFEM_NO_SMALL=1, the default for larger problems), with the LDG
     kernels (HPFEM_NO_TMA=1, also the fallback for shapes TMA cannot express)
     and with the transposed solve forced (HPFEM_TRANSPOSE=1, reading R23; TMA
-    or LDG kernels as the transposed shape allows)."""
+    or LDG kernels as the transposed shape allows).  plan.path() reports what
+    ran."""
     for k in ("HPFEM_NO_TMA", "HPFEM_NO_SMALL", "HPFEM_TRANSPOSE"):
         monkeypatch.delenv(k, raising=False)
     if request.param != "small":
