@@ -276,7 +276,11 @@ int hpfem_plan_launches(hpfem_plan_t plan, long long* launches);
  * 2 = final W C^{-1} kernels, 3 = load K8, 4 = apply K7), the summed
  * duration ms[k], launch count n[k] and algorithmic HBM bytes bytes[k]
  * (DESIGN.md "Roofline"), then resets the counters.  Events beyond the
- * capacity are not recorded (n[] tells).
+ * capacity are not recorded (n[] tells).  Profiling keeps the launch
+ * configuration of an unprofiled solve (the TMA half-steps' hat lines still
+ * run concurrently on the side stream and are then in no kind) but launches
+ * the kernels directly instead of replaying the solve's CUDA graph, and
+ * disables the one-CTA solve K11 (its passes are not separate kernels).
  */
 int hpfem_plan_profile(hpfem_plan_t plan, int capacity);
 int hpfem_plan_profile_read(hpfem_plan_t plan, double* ms /*[5]*/, long long* n /*[5]*/, double* bytes /*[5]*/);

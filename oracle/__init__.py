@@ -72,6 +72,8 @@ def _declare(L):
     L.oracle_unload.argtypes = [_dp, _i, _i, _dp, _i, _i, _i, _dp, _dp]
     L.oracle_set_robin.argtypes = [_dp]
     L.oracle_set_robin.restype = None
+    L.oracle_set_threads.argtypes = [_i]
+    L.oracle_set_threads.restype = None
     for f in ("oracle_operator_dense", "oracle_operator_coo", "oracle_factor_dense", "oracle_solve1d",
               "oracle_spectrum", "oracle_shifts", "oracle_plan", "oracle_adi_solve", "oracle_apply", "oracle_load", "oracle_unload"):
         getattr(L, f).restype = _i
@@ -99,6 +101,11 @@ def _f64(a):
 def threads():
     """OpenMP threads used by the oracle's line loops."""
     return lib().oracle_threads()
+
+
+def set_threads(n: int):
+    """OpenMP threads of the line loops (n <= 0: all host cores)."""
+    lib().oracle_set_threads(n)
 
 
 class robin:

@@ -696,6 +696,14 @@ void oracle_set_robin(const double* alpha4) {
 /* OpenMP threads the oracle's line loops use (bench.py cpu_baseline.cores) */
 int oracle_threads(void) { return omp_get_max_threads(); }
 
+/* Set the OpenMP thread count of the line loops (n <= 0: the default, all
+ * host cores).  Test / baseline infrastructure only: bench.py times a
+ * single-threaded sample next to the all-core run. */
+void oracle_set_threads(int n) {
+  static const int dflt = omp_get_max_threads();
+  omp_set_num_threads(n > 0 ? n : dflt);
+}
+
 /* N of the 1D space */
 int oracle_dim(int n, int p, int bc) {
   const int nh = n + 1 - ((bc == 0 || bc == 2) ? 1 : 0) - ((bc == 0 || bc == 3) ? 1 : 0);

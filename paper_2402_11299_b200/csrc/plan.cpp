@@ -738,11 +738,13 @@ int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st,
   int rc;
   const int e0 = prof_mark(pl, st);
   // Concurrent hat lines: the persistent TMA grid leaves `spare` SMs to the
-  // hat-line kernel on the side stream (serial when profiling, so that the
-  // per-kind times stay attributable).  HPFEM_HAT_SMS sets `spare` (0 = serial).
+  // hat-line kernel on the side stream.  HPFEM_HAT_SMS sets `spare` (0 =
+  // serial).  When profiling, the event after the bubble kernel is recorded
+  // on the launch stream before the join, so it times the bubble kernel alone
+  // in the same concurrent configuration (the hat lines are in no kind).
   P.tun = pl->tun;
   const int spare_env = pl->tun.hat_sms;
-  if (tma_supports(w.tma, P.dir) && P.o.nh > 0 && spare_env > 0 && e0 < 0 && pl->ev.empty() && w.hs) {
+  if (tma_supports(w.tma, P.dir) && P.o.nh > 0 && spare_env > 0 && w.hs) {
     StepParams H = P;
     H.lp_begin = P.dir == 0 ? 0 : P.o.nb;
     H.lp_count = P.o.nh;
@@ -750,6 +752,7 @@ int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st,
     if ((ce = cudaEventRecord(w.hfork, st)) != cudaSuccess) return cuda_err(ce, "fork");
     rc = count_launch(pl, tma_launch_step(w.tma, P, ia_g, ia_w, st, spare_env), "TMA bubble kernel");
     if (rc) return rc;
+    prof_add(pl, k0, e0, prof_mark(pl, st), per * (double)P.o.nb * P.s.nb);
     if ((ce = cudaStreamWaitEvent(w.hs, w.hfork, 0)) != cudaSuccess) return cuda_err(ce, "fork");
     rc = count_launch(pl, launch_hat_lines(H, w.hs), "hat-line kernel");
     if (rc) return rc;
