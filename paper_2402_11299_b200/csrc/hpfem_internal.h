@@ -118,7 +118,9 @@ inline Layout make_layout(const DirDev& y, int emaj) {
  * plans on several host threads / devices do not race (defaults in
  * parentheses; all are experiment knobs). */
 struct Tuning {
-  int hat_sms;        // HPFEM_HAT_SMS (4): SMs the persistent TMA grid leaves to the side-stream hat lines
+  int hat_sms;        // HPFEM_HAT_SMS (-1): SMs the persistent TMA grid leaves to the side-stream hat lines
+                      // (0: hat lines serial on the launch stream; < 0: side stream, no SMs reserved --
+                      // they fill the bubble kernel's tail; 1, 2, 4, 8 measured the same total at config 5)
   int no_graph;       // HPFEM_NO_GRAPH (0)
   int no_small;       // HPFEM_NO_SMALL (0)
   int no_tma;         // HPFEM_NO_TMA (0)

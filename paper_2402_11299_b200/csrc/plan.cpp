@@ -60,7 +60,7 @@ int env_int(const char* name, int dflt) {
 /* the tuning switches (hpfem_internal.h Tuning), read once per plan */
 Tuning read_tuning() {
   Tuning t;
-  t.hat_sms = env_int("HPFEM_HAT_SMS", 4);
+  t.hat_sms = env_int("HPFEM_HAT_SMS", -1);
   t.no_graph = env_int("HPFEM_NO_GRAPH", 0) == 1;
   t.no_small = env_int("HPFEM_NO_SMALL", 0) == 1;
   t.no_tma = env_int("HPFEM_NO_TMA", 0) == 1;
@@ -744,13 +744,14 @@ int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st,
   // in the same concurrent configuration (the hat lines are in no kind).
   P.tun = pl->tun;
   const int spare_env = pl->tun.hat_sms;
-  if (tma_supports(w.tma, P.dir) && P.o.nh > 0 && spare_env > 0 && w.hs) {
+  if (tma_supports(w.tma, P.dir) && P.o.nh > 0 && spare_env != 0 && w.hs) {
     StepParams H = P;
     H.lp_begin = P.dir == 0 ? 0 : P.o.nb;
     H.lp_count = P.o.nh;
     cudaError_t ce;
     if ((ce = cudaEventRecord(w.hfork, st)) != cudaSuccess) return cuda_err(ce, "fork");
-    rc = count_launch(pl, tma_launch_step(w.tma, P, ia_g, ia_w, st, spare_env), "TMA bubble kernel");
+    rc = count_launch(pl, tma_launch_step(w.tma, P, ia_g, ia_w, st, spare_env > 0 ? spare_env : 0),
+                      "TMA bubble kernel");
     if (rc) return rc;
     prof_add(pl, k0, e0, prof_mark(pl, st), per * (double)P.o.nb * P.s.nb);
     if ((ce = cudaStreamWaitEvent(w.hs, w.hfork, 0)) != cudaSuccess) return cuda_err(ce, "fork");
