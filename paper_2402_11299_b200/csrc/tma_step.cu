@@ -124,6 +124,34 @@ struct TmaStepArgs {
   FDiv fS, fN, fG, fT;  // divisions by S, NST, #element groups, and x.n (x-solve) / nwt (y-solve)
 };
 
+/* HPFEM_CHECKS (debug builds: HPFEM_NVCC_EXTRA=-DHPFEM_CHECKS): device-side
+ * bounds checks of the ring / tile bookkeeping (trap on violation) and a NaN
+ * poison of the whole ring before the first TMA issue, so that a stage read
+ * before its bytes landed propagates NaN into the solution (the parity tests
+ * then fail).  compute-sanitizer is closed on this pool; this is the
+ * substitute (tests/test_gpu_parity.py, scripts/r2_checks.sh). */
+#ifdef HPFEM_CHECKS
+#define HPFEM_CHECK(cond) \
+  do {                    \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define HPFEM_CHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
+__device__ __forceinline__ void poison_ring(unsigned char* ring, int bytes) {
+#ifdef HPFEM_CHECKS
+  double* r = reinterpret_cast<double*>(ring);
+  for (int i = threadIdx.x; i < bytes / 8; i += blockDim.x) r[i] = __longlong_as_double(0x7ff8dead0000beefLL);
+  fence_proxy_async();  // the generic-proxy poison before the async-proxy (TMA) fills
+#else
+  (void)ring;
+  (void)bytes;
+#endif
+}
+
 constexpr int NT = 256;    // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int KR = 8;      // x-solve: chain positions (rows) per stage
@@ -188,6 +216,8 @@ __device__ __forceinline__ void x_issue(const TmaStepArgs& A, uint32_t gs, unsig
   const int slot = (int)(gs - A.fN.div(gs) * A.nstages);
   const int rest = (int)A.fG.div(tile), g = tile - rest * (int)A.fG.d;
   const int pi = (int)A.fT.div(rest), e_x = rest - pi * x.n;
+  HPFEM_CHECK(slot >= 0 && slot < A.nstages && s >= 0 && s < A.S && pi >= 0 && pi < 2 && e_x >= 0 && e_x < x.n &&
+              g >= 0 && g * A.EG < y.n && A.tx_bytes <= A.stage_bytes);
   const int EG = A.EG;
   const int c0 = P.lay.hb + g * EG * P.lay.Q;
   const int hc = (g * EG - drop_left(y.bc)) & ~1;  // innermost TMA coordinate: 16-byte aligned
@@ -237,6 +267,7 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
     for (int k = 0; k < NST; ++k) mbar_init(&full[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  poison_ring(ring, NST * A.stage_bytes);
   __syncthreads();
   if (threadIdx.x == 0)
     for (int k = 0; k < NST; ++k) x_issue<MODE>(A, k, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
@@ -431,6 +462,9 @@ __device__ __forceinline__ void y_issue(const TmaStepArgs& A, uint32_t gs, unsig
   if (tile >= A.ntiles) return;
   const int slot = (int)(gs - A.fN.div(gs) * A.nstages);
   const YTile t = y_decode(A, tile);
+  HPFEM_CHECK(slot >= 0 && slot < A.nstages && s >= 0 && s < A.S && t.pi >= 0 && t.pi < 2 && t.e_x >= 0 &&
+              t.e_x < x.n && t.g >= 0 && t.g * A.EG < y.n && t.kw * A.R < chain_len(x.p, t.pi) &&
+              A.tx_bytes <= A.stage_bytes);
   const int e0 = t.g * A.EG, kh0 = t.kw * A.R;
   const int hL = t.e_x - drop_left(x.bc);
   unsigned char* st = ring + (size_t)slot * A.stage_bytes;
@@ -485,6 +519,7 @@ __global__ void __launch_bounds__(NT, 1)
     for (int k = 0; k < NST; ++k) mbar_init(&full[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  poison_ring(ring, NST * A.stage_bytes);
   __syncthreads();
   if (threadIdx.x == 0)
     for (int k = 0; k < NST; ++k) y_issue<MODE>(A, k, ring, full, &mG0, &mG1, &mW0, &mW1, &mH, fbuf);

@@ -601,3 +601,45 @@ def test_two_host_threads_bitwise():
     for k in range(2):
         for U in out[k]:
             assert np.array_equal(U, refs[k])
+
+
+def test_tma_ring_stress_bitwise(monkeypatch):
+    """Race evidence for the lock-free TMA ring (tma_step.cu release_is_last:
+    acq_rel shared counters, proxy fences, last releaser refills; the
+    compute-sanitizer tools are closed on this pool): the same solves with
+    ring depths NST = 1 .. 4, with 0 / 8 SMs left to the side-stream hat
+    lines (a different tile -> CTA assignment) and with the hat lines on the
+    launch stream, repeated 8 times each, are all bitwise identical -- the
+    per-thread arithmetic does not depend on any of these, so a missed fence
+    or an early slot refill would show as a difference."""
+    torch = torch_cuda()
+    c = W.CONFIGS[2]
+    xs2, ys2 = c.breakpoints()
+    cases = [(xs2, c.px, ys2, c.py, c.omega, c.bc, c.tol), SMALL[17], SMALL[19]]
+    envs = [{}, {"HPFEM_NST_X": "1", "HPFEM_NST_Y": "1"}, {"HPFEM_NST_X": "2", "HPFEM_NST_Y": "2"},
+            {"HPFEM_NST_X": "3", "HPFEM_NST_Y": "3"}, {"HPFEM_HAT_SMS": "8"}, {"HPFEM_HAT_SMS": "0"},
+            {"HPFEM_HAT_SMS": "-1", "HPFEM_NO_GRAPH": "1"}]
+    for k, (xs, px, ys, py, om, bc, tol) in enumerate(cases):
+        G = W.random_field((oracle.dim(len(xs) - 1, px, oracle.split_bc(bc)[0]),
+                            oracle.dim(len(ys) - 1, py, oracle.split_bc(bc)[1])), 500 + k)
+        ref = None
+        for env in envs:
+            for key in ("HPFEM_NST_X", "HPFEM_NST_Y", "HPFEM_HAT_SMS", "HPFEM_NO_GRAPH", "HPFEM_NO_SMALL"):
+                monkeypatch.delenv(key, raising=False)
+            monkeypatch.setenv("HPFEM_NO_SMALL", "1")
+            for key, v in env.items():
+                monkeypatch.setenv(key, v)
+            plan = gpu_plan(xs, px, ys, py, om, bc, tol)
+            assert plan.path()["path"] == "tma"
+            Gd = torch.from_numpy(G).cuda()
+            Ud = torch.empty_like(Gd)
+            for rep in range(8):
+                Ud.fill_(float("nan"))
+                plan.solve(Gd, Ud)
+                U = Ud.cpu().numpy()
+                if ref is None:
+                    ref = U
+                    fl, Uref = oracle_reference(plan, xs, px, ys, py, om, bc, tol, G, floor=False)
+                    assert parity(xs, px, ys, py, bc, U, Uref)[0] <= L2_TOL
+                assert np.array_equal(U, ref), (k, env, rep)
+            plan.close()

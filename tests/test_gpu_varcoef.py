@@ -108,7 +108,12 @@ def test_pcg_table1(m, p):
     # (measured 2e-12 at m=3, p=64 and 1.5e-11 at p=128): bar 1e-10 = 1% of rtol
     assert rel <= GOLDEN["rtol"] and abs(rel - hist[-1]) <= 1e-10
     l2 = parity(xs, p, xs, p, 0, U, Uref)[0]
-    assert l2 <= 1e-10
+    # 1e-10, or 10x the oracle PCG's own rounding floor where that is larger
+    # (m = 3, p = 128: the oracle vs itself under a 1e-16 perturbation of b
+    # moves by 7e-11; scripts/pcg_floor.py, reading R24)
+    fl = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "pcg_floor.json")))[f"{m}-{p}"]
+    print(f"   L2 {l2:.2e} (oracle floor {fl['G_perturb_l2']:.1e})")
+    assert l2 <= max(1e-10, 10 * fl["G_perturb_l2"])
     r = b - T.varcoef_apply(xs, p, xs, p, 0, cg, U)  # the true residual of the GPU's U
     assert abs(np.linalg.norm(r) / np.linalg.norm(b) - rel) <= 1e-10
     plan.close()
