@@ -1114,63 +1114,116 @@ __device__ __forceinline__ void hat_tables(const StepParams& P, double* fil, dou
   }
 }
 
-/* y-solves (DIR 1): lines = rows, one warp per row, lane L owns the hats
- * [L HB, L HB + HB) (contiguous in the row: coalesced loads / stores) */
+/* y-solves (DIR 1): lines = rows, one warp per row.  Loads, right-hand
+ * sides and stores touch hat t = lane + 32 i (coalesced: a warp request is
+ * 256 contiguous bytes); the scan needs lane L to own the contiguous block
+ * [L HB, L HB + HB), so the right-hand sides are handed over through a
+ * per-warp shared-memory row (padded t + t/8: conflict-free in both
+ * orders).  With the blocked mapping for the loads as well, each request
+ * touched 31 sectors (ncu: L1-wavefront bound, 99 us at 255 hats). */
+__device__ __forceinline__ int hpad(int t) { return t + (t >> 3); }
+
 template <int HB>
 __global__ void __launch_bounds__(256, 2) k_hats_rows(StepParams P) {
-  __shared__ double fil[256], fhd[256], fhu[256], cpl[4 * 256];
+  constexpr int PADN = 32 * HB + 4 * HB;  // padded row length (hpad(32 HB - 1) < PADN)
+  __shared__ double fil[PADN], fhd[PADN], fhu[PADN];  // padded, read in the blocked order
+  __shared__ double cpl[4][32 * HB];                  // couplings [k][t], read in the strided order
+  __shared__ double rs[8][PADN];                      // per-warp row handover
   const DirDev& s = P.s;
   const int nh = s.nh, n = s.n, ld = P.ld, dl = drop_left(s.bc);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int t0 = lane * HB;
   const bool k1 = s.p - 2 >= 1;
-  hat_tables(P, fil, fhd, fhu, cpl);
+  {
+    const double S = P.f.sig;
+    for (int t = threadIdx.x; t < nh; t += blockDim.x) {
+      const double il = __ldg(P.f.ilh + t);
+      fil[hpad(t)] = il;
+      fhd[hpad(t)] = __ldg(P.f.gh + t) * il;
+      fhu[hpad(t)] = (t > 0 ? __ldg(P.f.gh + t - 1) : 0.0) * il;
+      const int node = node_of_hat(t, s.bc);
+      const int eL = node - 1, eR = node;
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+      if (eL >= 0) {
+        const double dlt = s.delta[eL];
+        c0 = s_hat_bub(S, dlt, 1, 0);
+        if (k1) c1 = s_hat_bub(S, dlt, 1, 1);
+      }
+      if (eR <= n - 1) {
+        const double drt = s.delta[eR];
+        c2 = s_hat_bub(S, drt, 0, 0);
+        if (k1) c3 = s_hat_bub(S, drt, 0, 1);
+      }
+      cpl[0][t] = c0;
+      cpl[1][t] = c1;
+      cpl[2][t] = c2;
+      cpl[3][t] = c3;
+    }
+  }
   __syncthreads();
   const double* __restrict__ G = P.G;
   const double* __restrict__ Xp = P.Xp;
   const double aG = P.alphaG;
+  const bool anyW = P.mode != ST_NONE;
+  double* row = rs[w];
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int lp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; lp < P.o.N; lp += nwarps) {
     const int l = row_of(P.o, lp);
     Stencil st;
     line_stencil<1>(P, l, st);
-    // chain-first bubbles z(l, e, 0/1) of the elements e = t0 + dl - 1 .. t0 + dl + HB - 1
-    double2 zz[HB + 1];
+    // right-hand sides r_h - B z for t = lane + 32 i; all loads of a chunk of
+    // HC hats issued before the FMAs (absent stencil rows clamped, skipped)
+    constexpr int HC = HB < 4 ? HB : 2;  // no register spills at 128 registers
 #pragma unroll
-    for (int i = 0; i <= HB; ++i) {
-      int e = t0 + dl - 1 + i;
-      e = e < 0 ? 0 : (e > n - 1 ? n - 1 : e);  // absent elements have zero couplings
-      if (P.z01) {
-        zz[i] = __ldg(reinterpret_cast<const double2*>(P.z01 + (size_t)l * 2 * n + 2 * e));
-      } else {
-        zz[i].x = __ldg(P.out + (size_t)l * ld + ycol_ke(P.lay, 0, e));
-        zz[i].y = k1 ? __ldg(P.out + (size_t)l * ld + ycol_ke(P.lay, 1, e)) : 0.0;
-      }
-    }
-    double r[HB];
+    for (int i0 = 0; i0 < HB; i0 += HC) {
+      double gv[HC], xv[7][HC];
+      double2 zl[HC], zr[HC];
 #pragma unroll
-    for (int i = 0; i < HB; ++i) {
-      const int t = t0 + i;
-      double rh = 0.0;
-      if (t < nh) {
-        if (aG != 0.0) rh = aG * __ldg(G + (size_t)l * ld + t);
+      for (int u = 0; u < HC; ++u) {
+        const int t = min(lane + 32 * (i0 + u), nh - 1);
+        gv[u] = aG != 0.0 ? __ldg(G + (size_t)l * ld + t) : 0.0;
 #pragma unroll
         for (int q = 0; q < 7; ++q)
-          if (st.idx[q] >= 0) rh += st.w[q] * __ldg(Xp + (size_t)st.idx[q] * ld + t);
-        const double* c = cpl + 4 * t;
-        rh -= c[0] * zz[i].x;
-        if (k1) rh -= c[1] * zz[i].y;
-        rh -= c[2] * zz[i + 1].x;
-        if (k1) rh -= c[3] * zz[i + 1].y;
+          xv[q][u] = anyW ? __ldg(Xp + (size_t)(st.idx[q] >= 0 ? st.idx[q] : l) * ld + t) : 0.0;
+        const int node = t + dl;
+        const int eL = max(node - 1, 0), eR = min(node, n - 1);  // absent elements: zero couplings
+        if (P.z01) {
+          zl[u] = __ldg(reinterpret_cast<const double2*>(P.z01 + (size_t)l * 2 * n + 2 * eL));
+          zr[u] = __ldg(reinterpret_cast<const double2*>(P.z01 + (size_t)l * 2 * n + 2 * eR));
+        } else {
+          zl[u].x = __ldg(P.out + (size_t)l * ld + ycol_ke(P.lay, 0, eL));
+          zl[u].y = k1 ? __ldg(P.out + (size_t)l * ld + ycol_ke(P.lay, 1, eL)) : 0.0;
+          zr[u].x = __ldg(P.out + (size_t)l * ld + ycol_ke(P.lay, 0, eR));
+          zr[u].y = k1 ? __ldg(P.out + (size_t)l * ld + ycol_ke(P.lay, 1, eR)) : 0.0;
+        }
       }
-      r[i] = rh;
+#pragma unroll
+      for (int u = 0; u < HC; ++u) {
+        const int i = i0 + u, t = lane + 32 * i;
+        if (i >= HB) break;
+        if (t < nh) {
+          double rh = aG != 0.0 ? aG * gv[u] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 7; ++q)
+            if (st.idx[q] >= 0) rh += st.w[q] * xv[q][u];
+          rh -= cpl[0][t] * zl[u].x;
+          if (k1) rh -= cpl[1][t] * zl[u].y;
+          rh -= cpl[2][t] * zr[u].x;
+          if (k1) rh -= cpl[3][t] * zr[u].y;
+          row[hpad(t)] = rh;
+        }
+      }
     }
+    __syncwarp();
+    double r[HB];
+#pragma unroll
+    for (int i = 0; i < HB; ++i) r[i] = t0 + i < nh ? row[hpad(t0 + i)] : 0.0;
     // down sweep: block map, suffix scan over the lanes, local sweep
     Aff f{0.0, 1.0};
 #pragma unroll
     for (int i = HB - 1; i >= 0; --i) {
       const int t = t0 + i;
-      if (t < nh) f = Aff{fma(-fhd[t], f.a, fil[t] * r[i]), -fhd[t] * f.b};
+      if (t < nh) f = Aff{fma(-fhd[hpad(t)], f.a, fil[hpad(t)] * r[i]), -fhd[hpad(t)] * f.b};
     }
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1183,16 +1236,16 @@ __global__ void __launch_bounds__(256, 2) k_hats_rows(StepParams P) {
     for (int i = HB - 1; i >= 0; --i) {
       const int t = t0 + i;
       if (t < nh) {
-        v = fma(-fhd[t], v, fil[t] * r[i]);
+        v = fma(-fhd[hpad(t)], v, fil[hpad(t)] * r[i]);
         r[i] = v;
       }
     }
-    // up sweep: block map, prefix scan, local sweep and store
+    // up sweep: block map, prefix scan, local sweep
     f = Aff{0.0, 1.0};
 #pragma unroll
     for (int i = 0; i < HB; ++i) {
       const int t = t0 + i;
-      if (t < nh) f = Aff{fma(-fhu[t], f.a, fil[t] * r[i]), -fhu[t] * f.b};
+      if (t < nh) f = Aff{fma(-fhu[hpad(t)], f.a, fil[hpad(t)] * r[i]), -fhu[hpad(t)] * f.b};
     }
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1201,15 +1254,22 @@ __global__ void __launch_bounds__(256, 2) k_hats_rows(StepParams P) {
     }
     v = __shfl_up_sync(0xffffffffu, f.a, 1);
     if (lane == 0) v = 0.0;
-    double* __restrict__ out = P.out + (size_t)l * ld;
 #pragma unroll
     for (int i = 0; i < HB; ++i) {
       const int t = t0 + i;
       if (t < nh) {
-        v = fma(-fhu[t], v, fil[t] * r[i]);
-        out[t] = v;
+        v = fma(-fhu[hpad(t)], v, fil[hpad(t)] * r[i]);
+        row[hpad(t)] = v;
       }
     }
+    __syncwarp();
+    double* __restrict__ out = P.out + (size_t)l * ld;
+#pragma unroll
+    for (int i = 0; i < HB; ++i) {
+      const int t = lane + 32 * i;
+      if (t < nh) out[t] = row[hpad(t)];
+    }
+    __syncwarp();  // the row buffer is rewritten by the next row
   }
 }
 
@@ -1221,7 +1281,7 @@ __host__ __device__ constexpr size_t hats_cols_smem_doubles(int nh) {
   return (size_t)nh * HC_COLS + 7 * (size_t)nh + 2 * 8 * HC_COLS;
 }
 
-__global__ void __launch_bounds__(256, 4) k_hats_cols(StepParams P) {
+__global__ void __launch_bounds__(256, 2) k_hats_cols(StepParams P) {
   extern __shared__ double sh[];
   const DirDev& s = P.s;
   const int nh = s.nh, n = s.n, ld = P.ld, dl = drop_left(s.bc);
@@ -1247,24 +1307,40 @@ __global__ void __launch_bounds__(256, 4) k_hats_cols(StepParams P) {
     const double* __restrict__ Xp = P.Xp;
     const double* __restrict__ Z = P.out;  // chain-first bubbles of this half-step
     const double aG = P.alphaG;
-#pragma unroll 4
-    for (int t = ta; t < tb; ++t) {
-      const int node = t + dl;
-      const int eL = max(node - 1, 0), eR = min(node, n - 1);  // absent: zero coupling
-      const double zl0 = __ldg(Z + (size_t)(s.nh + eL) * ld + li);
-      const double zr0 = __ldg(Z + (size_t)(s.nh + eR) * ld + li);
-      const double zl1 = k1 ? __ldg(Z + (size_t)(s.nh + n + eL) * ld + li) : 0.0;
-      const double zr1 = k1 ? __ldg(Z + (size_t)(s.nh + n + eR) * ld + li) : 0.0;
-      double rh = aG != 0.0 ? aG * __ldg(G + (size_t)t * ld + li) : 0.0;
+    // chunks of 2 hats, all loads of a chunk issued before the FMAs (as
+    // k_hats_rows: absent stencil columns clamped, their terms skipped)
+    const bool anyW = P.mode != ST_NONE;
+    for (int t0 = ta; t0 < tb; t0 += 2) {
+      double zv[2][4], gv[2], xv[7][2];
 #pragma unroll
-      for (int q = 0; q < 7; ++q)
-        if (st.idx[q] >= 0) rh += st.w[q] * __ldg(Xp + (size_t)t * ld + st.idx[q]);
-      const double* c = cpl + 4 * t;
-      rh -= c[0] * zl0;
-      if (k1) rh -= c[1] * zl1;
-      rh -= c[2] * zr0;
-      if (k1) rh -= c[3] * zr1;
-      v[t * HC_COLS + lane] = rh;
+      for (int u = 0; u < 2; ++u) {
+        const int t = min(t0 + u, tb - 1);
+        const int node = t + dl;
+        const int eL = max(node - 1, 0), eR = min(node, n - 1);  // absent: zero coupling
+        zv[u][0] = __ldg(Z + (size_t)(s.nh + eL) * ld + li);
+        zv[u][1] = k1 ? __ldg(Z + (size_t)(s.nh + n + eL) * ld + li) : 0.0;
+        zv[u][2] = __ldg(Z + (size_t)(s.nh + eR) * ld + li);
+        zv[u][3] = k1 ? __ldg(Z + (size_t)(s.nh + n + eR) * ld + li) : 0.0;
+        gv[u] = aG != 0.0 ? __ldg(G + (size_t)t * ld + li) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+          xv[q][u] = anyW ? __ldg(Xp + (size_t)t * ld + (st.idx[q] >= 0 ? st.idx[q] : li)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int t = t0 + u;
+        if (t >= tb) break;
+        double rh = aG != 0.0 ? aG * gv[u] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+          if (st.idx[q] >= 0) rh += st.w[q] * xv[q][u];
+        const double* c = cpl + 4 * t;
+        rh -= c[0] * zv[u][0];
+        if (k1) rh -= c[1] * zv[u][1];
+        rh -= c[2] * zv[u][2];
+        if (k1) rh -= c[3] * zv[u][3];
+        v[t * HC_COLS + lane] = rh;
+      }
     }
   }
   // down sweep

@@ -201,7 +201,7 @@ __device__ __forceinline__ bool release_is_last(uint32_t* cnt, int slot) {
 /* tile = (x-element e_x, x-parity pi, group of EG y-elements); stage  */
 /* s = chain positions [KR s, KR s + KR) of the x-chain (rows)         */
 /* ------------------------------------------------------------------ */
-template <int MODE>
+template <int MODE, bool SPILL>
 __device__ __forceinline__ void x_issue(const TmaStepArgs& A, uint32_t gs, unsigned char* ring, uint64_t* full,
                                         const CUtensorMap* mG0, const CUtensorMap* mG1, const CUtensorMap* mW0,
                                         const CUtensorMap* mW1, const CUtensorMap* mH0, const CUtensorMap* mH1,
@@ -235,6 +235,15 @@ __device__ __forceinline__ void x_issue(const TmaStepArgs& A, uint32_t gs, unsig
                 P.wtab + (size_t)g * EG * 5 * P.lay.Q, wbytes, &full[slot]);
   } else {
     mbar_expect_tx(&full[slot], A.tx_bytes);
+  }
+  if (SPILL) {  // long chains: the streamed boxes leave L2 first (the parked values stay)
+    const uint64_t pf = policy_evict_first();
+    if (MODE != ST_CORR) tma_load_3d_hint(st, pi ? mG1 : mG0, &full[slot], c0, e_x, row, pf);
+    if (MODE != ST_NONE) {
+      tma_load_3d_hint(st + A.off_w, pi ? mW1 : mW0, &full[slot], c0, e_x, row, pf);
+      tma_load_3d_hint(st + A.off_h, pi ? mH1 : mH0, &full[slot], hc, e_x, row, pf);
+    }
+    return;
   }
   if (MODE != ST_CORR) tma_load_3d(st, pi ? mG1 : mG0, &full[slot], c0, e_x, row);
   if (MODE != ST_NONE) {
@@ -270,7 +279,7 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
   poison_ring(ring, NST * A.stage_bytes);
   __syncthreads();
   if (threadIdx.x == 0)
-    for (int k = 0; k < NST; ++k) x_issue<MODE>(A, k, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
+    for (int k = 0; k < NST; ++k) x_issue<MODE, (CL > 64)>(A, k, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
   const int tid = threadIdx.x;
   const int eo = tid / Q, ky = tid - eo * Q;
   const int mS = chain_len(x.p, 0);  // stages per tile cover the longer (even) chain
@@ -335,13 +344,14 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
       }
       __syncwarp();
       if (lane == 0 && release_is_last(cnt, slot))
-        x_issue<MODE>(A, gs + NST, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
+        x_issue<MODE, (CL > 64)>(A, gs + NST, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
       ++gs;
       if (++cslot == NST) {
         cslot = 0;
         ++cround;
       }
     };
+    const uint64_t pkeep = CL > CR ? policy_evict_last() : 0;  // the parked values stay in L2
     if (CL > CR) {  // spilled stages (positions >= CR), rolled
 #pragma unroll 1
       for (int sg = CL / KR - 1; sg >= CR / KR; --sg) {
@@ -354,7 +364,7 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
             if (c < m) {
               const double2 f = *reinterpret_cast<const double2*>(fb + 4 * c);  // (il, hd)
               yv = fma(-f.y, yv, f.x * rv[kk]);
-              if (valid) outc[orow(c)] = yv;
+              if (valid) st_hint(outc + orow(c), yv, pkeep);
             }
           }
         }
@@ -399,7 +409,7 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
       if (CL > CR) {  // spilled positions, rolled; y loaded one batch ahead
         double yn[KR];
 #pragma unroll
-        for (int u = 0; u < KR; ++u) yn[u] = CR + u < m ? out[orow(CR + u)] : 0.0;
+        for (int u = 0; u < KR; ++u) yn[u] = CR + u < m ? ld_hint(out + orow(CR + u), pkeep) : 0.0;
 #pragma unroll 1
         for (int c0 = CR; c0 < m; c0 += KR) {
           double yc[KR];
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
 #pragma unroll
           for (int u = 0; u < KR; ++u) {
             const int c = c0 + KR + u;
-            yn[u] = c < m ? out[orow(c)] : 0.0;
+            yn[u] = c < m ? ld_hint(out + orow(c), pkeep) : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < KR; ++u) {
