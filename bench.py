@@ -394,7 +394,7 @@ def run_ours(args, cfg):
 
     # ---- roofline of the dominant kernel (half-step bubble kernel K2-K4)
     peak, peak_kind = measured_peak()
-    kb = prof["halfstep_bubbles"]
+    kb = {k: prof["halfstep_bubbles_x"][k] + prof["halfstep_bubbles_y"][k] for k in ("ms", "launches", "bytes")}
     achieved = kb["bytes"] / (kb["ms"] / 1e3) / 1e9 if kb["ms"] > 0 else None
     traffic, traffic_src = ncu_traffic(cfg.idx)
     total_kernel_ms = sum(v["ms"] for v in prof.values())
@@ -409,6 +409,10 @@ def run_ours(args, cfg):
         "solve_alg_GBps": alg_bytes_step / (ms_per_step / 1e3) / 1e9,
         "solve_alg_frac": alg_bytes_step / (ms_per_step / 1e3) / 1e9 / peak,
         "per_kind_ms": {k: round(v["ms"] / args.steps, 4) for k, v in prof.items()},
+        "per_direction": {d: {"avg_launch_ms": v["ms"] / max(v["launches"], 1), "launches": v["launches"],
+                              "GBps": v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None,
+                              "frac": v["bytes"] / (v["ms"] / 1e3) / 1e9 / peak if v["ms"] > 0 else None}
+                          for d, v in (("x_solves", prof["halfstep_bubbles_x"]), ("y_solves", prof["halfstep_bubbles_y"]))},
         "per_kind_source": ("CUDA events around every launch on the launch stream, in the timed configuration "
                             "(hat lines concurrent on the side stream: in neither kind; no graph replay)"),
     }

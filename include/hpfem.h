@@ -272,8 +272,9 @@ int hpfem_plan_launches(hpfem_plan_t plan, long long* launches);
  * (bench.py's roofline).  hpfem_plan_profile(plan, capacity) creates
  * `capacity` events up front (0 disables and frees them).
  * hpfem_plan_profile_read synchronises on the last event and returns, per
- * kernel kind k (0 = half-step bubble kernel K2-K4, 1 = hat kernel K5,
- * 2 = final W C^{-1} kernels, 3 = load K8, 4 = apply K7), the summed
+ * kernel kind k (0 = bubble kernel K2-K4 of the half-steps A (y-solves),
+ * 1 = their hat Schur kernel K5, 2 = final W C^{-1} kernels, 3 = load K8,
+ * 4 = apply K7, 5 / 6 = as 0 / 1 for the half-steps B (x-solves)), the summed
  * duration ms[k], launch count n[k] and algorithmic HBM bytes bytes[k]
  * (DESIGN.md "Roofline"), then resets the counters.  Events beyond the
  * capacity are not recorded (n[] tells).  Profiling keeps the launch
@@ -283,7 +284,8 @@ int hpfem_plan_launches(hpfem_plan_t plan, long long* launches);
  * disables the one-CTA solve K11 (its passes are not separate kernels).
  */
 int hpfem_plan_profile(hpfem_plan_t plan, int capacity);
-int hpfem_plan_profile_read(hpfem_plan_t plan, double* ms /*[5]*/, long long* n /*[5]*/, double* bytes /*[5]*/);
+#define HPFEM_PROFILE_KINDS 7
+int hpfem_plan_profile_read(hpfem_plan_t plan, double* ms /*[7]*/, long long* n /*[7]*/, double* bytes /*[7]*/);
 
 void hpfem_plan_destroy(hpfem_plan_t plan);
 

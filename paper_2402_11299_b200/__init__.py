@@ -327,7 +327,7 @@ def hpfem_plan_launches(plan: int) -> int:
     return n.value
 
 
-KINDS = ("halfstep_bubbles", "halfstep_hats", "final", "load", "apply")
+KINDS = ("halfstep_bubbles_y", "halfstep_hats_y", "final", "load", "apply", "halfstep_bubbles_x", "halfstep_hats_x")
 
 
 def hpfem_plan_profile(plan: int, capacity: int):
@@ -335,9 +335,9 @@ def hpfem_plan_profile(plan: int, capacity: int):
 
 
 def hpfem_plan_profile_read(plan: int) -> dict:
-    ms = (ctypes.c_double * 5)()
-    n = (ctypes.c_longlong * 5)()
-    by = (ctypes.c_double * 5)()
+    ms = (ctypes.c_double * len(KINDS))()
+    n = (ctypes.c_longlong * len(KINDS))()
+    by = (ctypes.c_double * len(KINDS))()
     _check(_load().hpfem_plan_profile_read(plan, ms, n, by))
     return {k: dict(ms=ms[i], launches=n[i], bytes=by[i]) for i, k in enumerate(KINDS)}
 

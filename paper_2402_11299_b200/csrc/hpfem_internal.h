@@ -132,6 +132,7 @@ struct Tuning {
   int eg_y;           // HPFEM_EG_Y (0 = automatic): y-solve tile width
   int fake_stencil;   // HPFEM_FAKE_STENCIL (0): experiment only
   int hats_seq;       // HPFEM_HATS_SEQ (0): the sequential one-thread-per-line hat Schur kernel (experiment / A-B)
+  int no_hat_split;   // HPFEM_NO_HAT_SPLIT (0): hat Schur solves of the side-stream hat lines on the launch stream
   int transpose;      // HPFEM_TRANSPOSE (-1 auto, 0 never, 1 always): solve the transposed equation (R23)
 };
 
@@ -172,6 +173,11 @@ struct StepParams {
    * right-hand side touch -- contiguous instead of 16 bytes out of every Q. */
   double* z01;         // y-solves: written for every row of out
   const double* z01p;  // x-solves: the copy belonging to Xp
+  /* hat Schur kernel K5 only: the lines it takes, as processing positions
+   * [hl_begin, hl_end) -- y-solves: row positions (row_of: the x-bubble rows
+   * first, [0, o.nb), then the x-hat rows); x-solves: internal columns (hats
+   * and padding [0, lay.hb), then the y-bubbles).  hl_end <= 0 (e.g. zero-initialised): every line. */
+  int hl_begin, hl_end;
   Tuning tun;          // host-side launch choices (not read by the kernels)
 };
 
@@ -180,6 +186,8 @@ cudaError_t launch_factor(const DirDev& d, const double* kap, const double* sig,
                           size_t stride, int* err, cudaStream_t st);
 cudaError_t launch_step_bubbles(const StepParams& P, cudaStream_t st);
 cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st);
+/* can launch_step_hats take a sub-range of the lines (hl_begin / hl_end)? */
+bool hats_split_ok(const StepParams& P);
 cudaError_t launch_hat_lines(const StepParams& P, cudaStream_t st);  // element-major layout only
 cudaError_t launch_copyin(const DirDev& x, const DirDev& y, const Layout& L, const double* G, double* Gp,
                           cudaStream_t st);

@@ -1167,7 +1167,8 @@ __global__ void __launch_bounds__(256, 2) k_hats_rows(StepParams P) {
   const bool anyW = P.mode != ST_NONE;
   double* row = rs[w];
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int lp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; lp < P.o.N; lp += nwarps) {
+  const int lp_hi = P.hl_end <= 0 ? P.o.N : P.hl_end;
+  for (int lp = (P.hl_end <= 0 ? 0 : P.hl_begin) + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); lp < lp_hi; lp += nwarps) {
     const int l = row_of(P.o, lp);
     Stencil st;
     line_stencil<1>(P, l, st);
@@ -1281,7 +1282,7 @@ __host__ __device__ constexpr size_t hats_cols_smem_doubles(int nh) {
   return (size_t)nh * HC_COLS + 7 * (size_t)nh + 2 * 8 * HC_COLS;
 }
 
-__global__ void __launch_bounds__(256, 2) k_hats_cols(StepParams P) {
+__global__ void __launch_bounds__(256, 2) k_hats_cols(StepParams P, int col_begin, int col_end) {
   extern __shared__ double sh[];
   const DirDev& s = P.s;
   const int nh = s.nh, n = s.n, ld = P.ld, dl = drop_left(s.bc);
@@ -1295,8 +1296,8 @@ __global__ void __launch_bounds__(256, 2) k_hats_cols(StepParams P) {
   double* fb = fa + 8 * HC_COLS;
   hat_tables(P, fil, fhd, fhu, cpl);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int li = blockIdx.x * HC_COLS + lane;
-  const int l = li < ld ? ydof_of_col(P.lay, P.o, li) : -1;
+  const int li = col_begin + blockIdx.x * HC_COLS + lane;  // columns [col_begin, col_end), col_end <= ld
+  const int l = li < col_end ? ydof_of_col(P.lay, P.o, li) : -1;
   const int BH = (nh + 7) >> 3;
   const int ta = w * BH, tb = min(nh, ta + BH);
   __syncthreads();
@@ -1375,10 +1376,17 @@ static cudaError_t launch_hats_rows(const StepParams& P, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int warps = P.o.N, blocks = (warps + 7) / 8;
+  const int warps = P.hl_end <= 0 ? P.o.N : P.hl_end - P.hl_begin, blocks = (warps + 7) / 8;
+  if (blocks <= 0) return cudaSuccess;
   const int grid = blocks < 2 * sms ? blocks : 2 * sms;  // one wave of 2 CTAs per SM, grid-stride over rows
   k_hats_rows<HB><<<grid, 256, 0, st>>>(P);
   return cudaGetLastError();
+}
+
+bool hats_split_ok(const StepParams& P) {
+  if (P.s.nh == 0 || P.tun.hats_seq) return false;
+  if (P.dir == 1) return P.s.nh <= 256;
+  return sizeof(double) * hats_cols_smem_doubles(P.s.nh) <= 200 * 1024;
 }
 
 cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st) {
@@ -1401,7 +1409,8 @@ cudaError_t launch_step_hats(const StepParams& P, cudaStream_t st) {
   if (P.dir == 0 && smem <= 200 * 1024) {
     cudaError_t e = smem_optin((const void*)k_hats_cols, smem);
     if (e != cudaSuccess) return e;
-    k_hats_cols<<<(P.ld + HC_COLS - 1) / HC_COLS, 256, smem, st>>>(P);
+    const int cb = P.hl_end <= 0 ? 0 : P.hl_begin, ce = P.hl_end <= 0 ? P.ld : P.hl_end;
+    if (ce > cb) k_hats_cols<<<(ce - cb + HC_COLS - 1) / HC_COLS, 256, smem, st>>>(P, cb, ce);
     return cudaGetLastError();
   }
   return P.dir == 0 ? launch_hats_dir<0>(P, st) : launch_hats_dir<1>(P, st);  // very many hats

@@ -76,6 +76,7 @@ Tuning read_tuning() {
   t.eg_y = env_int("HPFEM_EG_Y", 0);
   t.fake_stencil = env_int("HPFEM_FAKE_STENCIL", 0);
   t.hats_seq = env_int("HPFEM_HATS_SEQ", 0);
+  t.no_hat_split = env_int("HPFEM_NO_HAT_SPLIT", 0) == 1;
   t.transpose = env_int("HPFEM_TRANSPOSE", -1);
   return t;
 }
@@ -734,7 +735,7 @@ bool overlap(const void* a, const void* b, size_t bytes) {
 int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st, bool final_step, int ia_g,
              int ia_w) {
   const double per = 8.0 * ((P.alphaG != 0.0 ? 1 : 0) + (P.mode != ST_NONE ? 1 : 0) + 1);
-  const int k0 = final_step ? 2 : 0, k1 = final_step ? 2 : 1;
+  const int k0 = final_step ? 2 : (P.dir == 0 ? 5 : 0), k1 = final_step ? 2 : (P.dir == 0 ? 6 : 1);
   int rc;
   const int e0 = prof_mark(pl, st);
   // Concurrent hat lines: the persistent TMA grid leaves `spare` SMs to the
@@ -757,8 +758,26 @@ int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st,
     if ((ce = cudaStreamWaitEvent(w.hs, w.hfork, 0)) != cudaSuccess) return cuda_err(ce, "fork");
     rc = count_launch(pl, launch_hat_lines(H, w.hs), "hat-line kernel");
     if (rc) return rc;
+    // The hat Schur solves of those hat lines follow them on the side stream;
+    // the ones of the bubble lines need the bubble kernel only, so neither
+    // waits for the other (joined before the next half-step).
+    const bool split = P.s.nh > 0 && hats_split_ok(P) && !pl->tun.no_hat_split;
+    if (split) {
+      StepParams K = P;
+      K.hl_begin = P.dir == 1 ? P.o.nb : 0;
+      K.hl_end = P.dir == 1 ? P.o.N : P.lay.hb;
+      rc = count_launch(pl, launch_step_hats(K, w.hs), "hat kernel (hat lines)");
+      if (rc) return rc;
+      K.hl_begin = P.dir == 1 ? 0 : P.lay.hb;
+      K.hl_end = P.dir == 1 ? P.o.nb : P.ld;
+      const int e2 = prof_mark(pl, st);
+      rc = count_launch(pl, launch_step_hats(K, st), "hat kernel");
+      if (rc) return rc;
+      prof_add(pl, k1, e2, prof_mark(pl, st), per * (double)P.o.nb * P.s.nh);
+    }
     if ((ce = cudaEventRecord(w.hjoin, w.hs)) != cudaSuccess) return cuda_err(ce, "join");
     if ((ce = cudaStreamWaitEvent(st, w.hjoin, 0)) != cudaSuccess) return cuda_err(ce, "join");
+    if (split) return HPFEM_OK;
   } else if (tma_supports(w.tma, P.dir)) {
     rc = count_launch(pl, tma_launch_step(w.tma, P, ia_g, ia_w, st), "TMA bubble kernel");
     if (rc) return rc;
@@ -1584,7 +1603,7 @@ int hpfem_plan_profile(hpfem_plan_t pl, int capacity) {
 
 int hpfem_plan_profile_read(hpfem_plan_t pl, double* ms, long long* n, double* bytes) {
   if (!pl || !ms || !n || !bytes) return set_err(HPFEM_EINVAL, "null argument");
-  for (int k = 0; k < 5; ++k) {
+  for (int k = 0; k < HPFEM_PROFILE_KINDS; ++k) {
     ms[k] = 0.0;
     n[k] = 0;
     bytes[k] = 0.0;
