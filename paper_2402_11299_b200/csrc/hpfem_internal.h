@@ -37,7 +37,8 @@ struct DirDev {
  *                    y_c = il_c r_c - hd_c y_{c+1},   z_c = il_c y_c - hu_c z_{c-1},
  *                  and [4c+3] = il_c again, so that each sweep reads its two
  *                  factors with one 16-byte load: (il, hd) down, (hu, il) up;
- *                  cfs = 4 roundup8(chain_len(p, 0)) + 2 (spreads smem banks); the
+ *                  cfs = 4 roundup8(chain_len(p, 0)) + 2 (spreads smem banks; see
+ *                  fac_cfs for chains of more than 64 positions); the
  *                  positions past a chain up to the next multiple of 8 (the TMA
  *                  stage height) hold zero factors, so a stage-padded
  *                  recurrence step there yields exactly 0 with no select.
@@ -54,7 +55,15 @@ struct FacView {
   double kap, sig;
 };
 
-HD int fac_cfs(const DirDev& d) { return 4 * ((d.p / 2 + 7) & ~7) + 2; }
+/* Chains longer than 64 positions (p > 129) get tables over 128 positions and
+ * the spike coefficients of the two-threads-per-chain x half-step (tma_step.cu,
+ * k_xstep_tma2) behind them, at cf + fac_spk_off: for c < 64 the influence
+ * beta_c of the value entering the lower half on y_c (beta_63 = -hd_63,
+ * beta_c = -hd_c beta_{c+1}), for c >= 64 the influence gamma_c of z_63 on z_c
+ * (gamma_64 = -hu_64, gamma_c = -hu_c gamma_{c-1}). */
+HD int fac_cf_pos(const DirDev& d) { return d.p / 2 > 64 ? 128 : (d.p / 2 + 7) & ~7; }
+HD int fac_spk_off(const DirDev& d) { return 4 * fac_cf_pos(d) + 2; }
+HD int fac_cfs(const DirDev& d) { return fac_spk_off(d) + (d.p / 2 > 64 ? 128 : 0); }
 
 HD size_t fac_cf_off(const DirDev& d) {
   size_t s = 4 * (size_t)d.nb + 2 * (size_t)d.nh;
@@ -132,6 +141,7 @@ struct Tuning {
   int eg_y;           // HPFEM_EG_Y (0 = automatic): y-solve tile width
   int fake_stencil;   // HPFEM_FAKE_STENCIL (0): experiment only
   int hats_seq;       // HPFEM_HATS_SEQ (0): the sequential one-thread-per-line hat Schur kernel (experiment / A-B)
+  int no_x2;          // HPFEM_NO_X2 (0): long x chains by the one-thread kernel (upper half parked in the output row)
   int no_hat_split;   // HPFEM_NO_HAT_SPLIT (0): hat Schur solves of the side-stream hat lines on the launch stream
   int transpose;      // HPFEM_TRANSPOSE (-1 auto, 0 never, 1 always): solve the transposed equation (R23)
 };

@@ -107,6 +107,19 @@ __global__ void k_factor_chains(DirDev d, const double* __restrict__ kap, const 
       cf[4 * c + 3] = il[b];
       gprev = g[b];
     }
+    if (d.p / 2 > 64) {  // spike coefficients of the two-threads-per-chain x half-step (hpfem_internal.h)
+      double* spk = cf + fac_spk_off(d);
+      double bt = 1.0;
+      for (int c = 63; c >= 0; --c) {
+        bt = c < m ? -cf[4 * c + 1] * bt : 0.0;
+        spk[c] = bt;
+      }
+      double gm = 1.0;
+      for (int c = 64; c < 128; ++c) {
+        gm = c < m ? -cf[4 * c + 2] * gm : 0.0;
+        spk[c] = gm;
+      }
+    }
   }
   // v_side = T^{-1} (beta e_0): the chain-first bubble is the only one
   // coupled to the hats (W_0 / W_1, ops1d.h)

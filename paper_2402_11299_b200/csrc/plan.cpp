@@ -77,6 +77,7 @@ Tuning read_tuning() {
   t.fake_stencil = env_int("HPFEM_FAKE_STENCIL", 0);
   t.hats_seq = env_int("HPFEM_HATS_SEQ", 0);
   t.no_hat_split = env_int("HPFEM_NO_HAT_SPLIT", 0) == 1;
+  t.no_x2 = env_int("HPFEM_NO_X2", 0) == 1;
   t.transpose = env_int("HPFEM_TRANSPOSE", -1);
   return t;
 }

@@ -111,6 +111,7 @@ struct TmaStepArgs {
   int S;            // stages per tile (the same for every tile of a launch)
   int stage_bytes;  // bytes per ring stage (all boxes, 128-aligned)
   int off_w, off_h; // byte offsets of the W and hat boxes inside a stage
+  int hi_g, hi_w, hi_h;  // two-threads-per-chain x kernel: byte offsets of the upper-half boxes from the lower ones
   int tx_bytes;     // bytes the TMA delivers per stage
   int hw;           // hat box width (x-solve)
   int out_off;      // y-solve: byte offset of the two output staging buffers
@@ -432,6 +433,220 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
               out[orow(c)] = z;
             }
           }
+        }
+      }
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* x-solve, chains of 65 .. 128 positions: two threads per chain       */
+/* (round 2).  The lower half of a chain (positions 0-63) and its upper */
+/* half (64-127) are held by the two half-warps of a warp, 64 positions */
+/* in registers each, and swept concurrently: a first-order recurrence  */
+/* over a half is affine in the value entering it, so each half sweeps  */
+/* with entry 0 and the true entry (one shuffle at the end of the       */
+/* sweep) is added through the tabled influence coefficients (spike     */
+/* coefficients, hpfem_internal.h fac_spk_off):                         */
+/*   down: y_c = a_c + beta_c y_64  (c < 64),                           */
+/*   up:   z_c = u_c + gamma_c z_63 (c >= 64).                          */
+/* Both half-warps run the same instructions (the entry is 0 where it   */
+/* does not apply).  Same factors, same right-hand sides; the           */
+/* association of the products differs from the sequential sweep        */
+/* (rounding level, as the scan-form hat solves).  Against the          */
+/* one-thread variant above (CL = 128: upper half parked in the output  */
+/* row, rolled loops) nothing leaves the registers.                     */
+/* tile = (e_x, parity, EG y-elements = <= 128 columns); stage s =      */
+/* chain positions [8s, 8s+8) and [64+8s, 64+8s+8): two boxes per       */
+/* array, the upper ones shifted by 128 bytes modulo 256 so the two     */
+/* half-warps read different banks.                                     */
+/* ------------------------------------------------------------------ */
+constexpr int XH = 64;  // positions per half
+
+template <int MODE>
+__device__ __forceinline__ void x2_issue(const TmaStepArgs& A, uint32_t gs, unsigned char* ring, uint64_t* full,
+                                         const CUtensorMap* mG0, const CUtensorMap* mG1, const CUtensorMap* mW0,
+                                         const CUtensorMap* mW1, const CUtensorMap* mH0, const CUtensorMap* mH1,
+                                         double* fbuf) {
+  const StepParams& P = A.P;
+  const DirDev& x = P.s;
+  const DirDev& y = P.o;
+  const uint32_t tl = A.fS.div(gs);
+  const int s = A.S - 1 - (int)(gs - tl * A.S);
+  const int tile = blockIdx.x + (int)tl * gridDim.x;
+  if (tile >= A.ntiles) return;
+  const int slot = (int)(gs - A.fN.div(gs) * A.nstages);
+  const int rest = (int)A.fG.div(tile), g = tile - rest * (int)A.fG.d;
+  const int pi = (int)A.fT.div(rest), e_x = rest - pi * x.n;
+  HPFEM_CHECK(slot >= 0 && slot < A.nstages && s >= 0 && s < A.S && pi >= 0 && pi < 2 && e_x >= 0 && e_x < x.n &&
+              g >= 0 && g * A.EG < y.n && A.tx_bytes <= A.stage_bytes);
+  const int EG = A.EG;
+  const int c0 = P.lay.hb + g * EG * P.lay.Q;
+  const int hc = (g * EG - drop_left(y.bc)) & ~1;
+  const int row = KR * s;  // rows past the chain: out of bounds, zero-filled (zero factors there)
+  unsigned char* st = ring + (size_t)slot * A.stage_bytes;
+  if (s == A.S - 1) {
+    const uint32_t fb = tl & 1;
+    const uint32_t fbytes = P.f.cfs * 8;
+    const int ne = (y.n - g * EG) < EG ? (y.n - g * EG) : EG;
+    const uint32_t wbytes = P.wtab ? ne * 5 * P.lay.Q * 8 : 0;
+    mbar_expect_tx(&full[slot], A.tx_bytes + fbytes + wbytes);
+    bulk_load(fbuf + fb * A.fac_doubles, P.f.cf + (size_t)(2 * e_x + pi) * P.f.cfs, fbytes, &full[slot]);
+    if (wbytes)
+      bulk_load(reinterpret_cast<unsigned char*>(fbuf) + (A.wb_off - A.fac_off) + fb * A.wb_doubles * 8,
+                P.wtab + (size_t)g * EG * 5 * P.lay.Q, wbytes, &full[slot]);
+  } else {
+    mbar_expect_tx(&full[slot], A.tx_bytes);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (MODE != ST_CORR) tma_load_3d(st + h * A.hi_g, pi ? mG1 : mG0, &full[slot], c0, e_x, row + h * XH);
+    if (MODE != ST_NONE) {
+      tma_load_3d(st + A.off_w + h * A.hi_w, pi ? mW1 : mW0, &full[slot], c0, e_x, row + h * XH);
+      tma_load_3d(st + A.off_h + h * A.hi_h, pi ? mH1 : mH0, &full[slot], hc, e_x, row + h * XH);
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, 1) k_xstep_tma2(const TmaStepArgs A, const __grid_constant__ CUtensorMap mG0,
+                                                      const __grid_constant__ CUtensorMap mG1,
+                                                      const __grid_constant__ CUtensorMap mW0,
+                                                      const __grid_constant__ CUtensorMap mW1,
+                                                      const __grid_constant__ CUtensorMap mH0,
+                                                      const __grid_constant__ CUtensorMap mH1) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const StepParams& P = A.P;
+  const DirDev& x = P.s;
+  const DirDev& y = P.o;
+  const int NST = A.nstages;
+  unsigned char* ring = smem_raw;
+  double* fbuf = reinterpret_cast<double*>(smem_raw + A.fac_off);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + A.bar_off);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(full + NST);
+  const int lane = threadIdx.x & 31;
+  const int EG = A.EG, q = y.p - 1, Q = P.lay.Q, BW = EG * Q;
+  const int ngroups = (y.n + EG - 1) / EG;
+  if (threadIdx.x < NST) cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NST; ++k) mbar_init(&full[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  poison_ring(ring, NST * A.stage_bytes);
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NST; ++k) x2_issue<MODE>(A, k, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
+  // thread -> (half h of the chain, column j of the tile)
+  const int h = lane >> 4, j = (threadIdx.x >> 5) * 16 + (lane & 15);
+  const int eo = j / Q, ky = j - eo * Q;
+  const int cb = h * XH;  // first chain position of this thread's half
+  const int spo = fac_spk_off(x);
+  int cslot = 0;
+  uint32_t cround = 0, ctt = 0, gs = 0;
+  for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++ctt) {
+    const int g = tile % ngroups, rest = tile / ngroups;
+    const int e_x = rest % x.n, pi = rest / x.n;
+    const int e0 = g * EG, ey = e0 + eo;
+    const int m = chain_len(x.p, pi);
+    const double* fb = fbuf + (ctt & 1) * A.fac_doubles;
+    const double* fbh = fb + 4 * cb;        // this half's factors
+    const double* sp = fb + spo + cb;       // this half's spike coefficients
+    const bool valid = j < BW && ky < q && ey < y.n;
+    const int h0 = (e0 - drop_left(y.bc)) & ~1;
+    Sten5 st;
+    int o0 = 0, o1 = 0, o2 = 0, o3 = 0, o4 = 0;
+    const bool wtab = P.wtab != nullptr && MODE == ST_APPLY;
+    const double* wb = reinterpret_cast<const double*>(smem_raw + A.wb_off) + (ctt & 1) * A.wb_doubles;
+    if (valid) {
+      if (!wtab) sten5_build(y, y.nh + ky * y.n + ey, MODE, P.kap_a, P.tau, P.cvL, P.cvR, st);
+      o0 = eo * Q + ky;
+      o1 = eo * Q + (ky >= 2 ? ky - 2 : ky);
+      o2 = eo * Q + (ky + 2 < q ? ky + 2 : ky);
+      const int hl = hat_of_node(ey, y.n, y.bc), hr = hat_of_node(ey + 1, y.n, y.bc);
+      o3 = (hl >= 0 ? hl : h0 + 1) - h0;
+      o4 = (hr >= 0 ? hr : h0 + 1) - h0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) st.w[k] = 0.0;
+    }
+    double ys[XH];
+    double yv = 0.0;
+    // down sweep of both halves, entry 0
+#pragma unroll
+    for (int sg = XH / KR - 1; sg >= 0; --sg) {
+      const int slot = cslot;
+      mbar_wait(&full[slot], cround & 1);
+      if (wtab && sg == XH / KR - 1) {  // first stage of the tile: the weights have landed
+#pragma unroll
+        for (int k = 0; k < 5; ++k) st.w[k] = valid ? wb[(eo * 5 + k) * Q + ky] : 0.0;
+      }
+      const unsigned char* stg = ring + (size_t)slot * A.stage_bytes;
+      const double* Gb = reinterpret_cast<const double*>(stg + h * A.hi_g);
+      const double* Wb = reinterpret_cast<const double*>(stg + A.off_w + h * A.hi_w);
+      const double* Hb = reinterpret_cast<const double*>(stg + A.off_h + h * A.hi_h);
+      double rv[KR];
+#pragma unroll
+      for (int kk = 0; kk < KR; ++kk) {
+        const double* Gs = Gb + kk * BW;
+        const double* Ws = Wb + kk * BW;
+        const double* Hs = Hb + kk * A.hw;
+        double r = 0.0;
+        if (MODE != ST_CORR) r = Gs[o0];
+        if (MODE != ST_NONE)
+          r += st.w[0] * Ws[o0] + st.w[1] * Ws[o1] + st.w[2] * Ws[o2] + st.w[3] * Hs[o3] + st.w[4] * Hs[o4];
+        rv[kk] = r;
+      }
+      __syncwarp();
+      if (lane == 0 && release_is_last(cnt, slot))
+        x2_issue<MODE>(A, gs + NST, ring, full, &mG0, &mG1, &mW0, &mW1, &mH0, &mH1, fbuf);
+      ++gs;
+      if (++cslot == NST) {
+        cslot = 0;
+        ++cround;
+      }
+#pragma unroll
+      for (int kk = KR - 1; kk >= 0; --kk) {
+        const int c = KR * sg + kk;
+        const double2 f = *reinterpret_cast<const double2*>(fbh + 4 * c);  // (il, hd); zero past the chain
+        yv = fma(-f.y, yv, f.x * rv[kk]);
+        ys[c] = yv;
+      }
+    }
+    // the value entering the lower half: y_64 of the upper half (0 for the upper half itself)
+    const double y64 = __shfl_sync(0xffffffffu, yv, (lane & 15) + 16);
+    const double e1 = h ? 0.0 : y64;
+    // up sweep of both halves, entry 0, on y_c = a_c + beta_c y_64
+    double z = 0.0;
+#pragma unroll
+    for (int c0 = 0; c0 < XH; c0 += KR) {
+      double2 fz[KR];
+      double sv[KR];
+#pragma unroll
+      for (int u = 0; u < KR; ++u) {
+        fz[u] = *reinterpret_cast<const double2*>(fbh + 4 * (c0 + u) + 2);  // (hu, il)
+        sv[u] = sp[c0 + u];
+      }
+#pragma unroll
+      for (int u = 0; u < KR; ++u) {
+        const int c = c0 + u;
+        z = fma(-fz[u].x, z, fz[u].y * fma(sv[u], e1, ys[c]));
+        ys[c] = z;
+      }
+    }
+    // the value entering the upper half: z_63 of the lower half
+    const double z63 = __shfl_sync(0xffffffffu, z, lane & 15);
+    const double e2 = h ? z63 : 0.0;
+    if (valid) {
+      double* __restrict__ out = P.out + P.lay.hb + (size_t)ey * Q + ky;
+#pragma unroll
+      for (int c0 = 0; c0 < XH; c0 += KR) {
+        double sv[KR];
+#pragma unroll
+        for (int u = 0; u < KR; ++u) sv[u] = sp[c0 + u];
+#pragma unroll
+        for (int u = 0; u < KR; ++u) {
+          const int c = cb + c0 + u;
+          if (c < m) out[(size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld] = fma(sv[u], e2, ys[c0 + u]);
         }
       }
     }
@@ -795,6 +1010,9 @@ struct TmaPlan {
   CUtensorMap xv[3][4];                 // x-solve views per array: [pi] bubble boxes, [2+pi] hat boxes
   CUtensorMap yG[3][2], yW[3][2], yH[3];
   CUtensorMap yO[2];                    // y-solve output stores (X1), per parity
+  bool x2ok = false;                    // two-threads-per-chain x kernel (chains of 65 .. 128 positions)
+  int EG2 = 0, hw2 = 0;
+  CUtensorMap xv2[3][4];                // its views: <= 128 columns per box
 };
 
 static int even_up(int v) { return (v + 1) & ~1; }
@@ -875,6 +1093,25 @@ TmaPlan* tma_plan_create(const DirDev& x, const DirDev& y, const Layout& L, doub
       const uint32_t b[3] = {(uint32_t)T->hw, 1, (uint32_t)KR};
       ok = encode(&T->xv[a][2 + pi], 3, base, d, s, b);
     }
+  }
+  // ---- x-solve views of the two-threads-per-chain kernel (<= 128 columns per tile)
+  if (chain_len(x.p, 0) > XH && L.Q <= 128) {
+    T->EG2 = 128 / L.Q < 1 ? 1 : 128 / L.Q;
+    if (T->EG2 > y.n) T->EG2 = y.n;
+    T->hw2 = even_up(T->EG2 + 2);
+    const int BW2 = T->EG2 * L.Q;
+    bool ok2 = true;
+    for (int a = 0; ok2 && a < 3; ++a)
+      for (int k = 0; ok2 && k < 4; ++k) {
+        const int pi = k & 1;
+        const int mpi = chain_len(x.p, pi) > 0 ? chain_len(x.p, pi) : 1;
+        double* base = arrays[a] + (size_t)(x.nh + pi * x.n) * L.ld;
+        const uint64_t d[3] = {(uint64_t)L.ld, (uint64_t)x.n, (uint64_t)mpi};
+        const uint64_t s[2] = {ld8, 2 * (uint64_t)x.n * ld8};
+        const uint32_t b[3] = {(uint32_t)(k < 2 ? BW2 : T->hw2), 1, (uint32_t)KR};
+        ok2 = encode(&T->xv2[a][k], 3, base, d, s, b);
+      }
+    T->x2ok = ok2;
   }
   // ---- y-solve views
   {
@@ -970,6 +1207,68 @@ static cudaError_t dispatch_y(int cl, const TmaStepArgs& A, const TmaPlan* T, in
 static int round128(int b) { return (b + 127) & ~127; }
 static int round1024(int b) { return (b + 1023) & ~1023; }
 
+template <int MODE>
+static cudaError_t launch_x2_mode(const TmaStepArgs& A, const CUtensorMap* g, const CUtensorMap* w, int grid,
+                                  size_t smem, cudaStream_t st) {
+  auto k = k_xstep_tma2<MODE>;
+  cudaError_t e = smem_optin((const void*)k, SMEM_OPTIN);
+  if (e != cudaSuccess) return e;
+  k<<<grid, NT, smem, st>>>(A, g[0], g[1], w[0], w[1], w[2], w[3]);
+  return cudaGetLastError();
+}
+
+/* x-solve with two threads per chain (A.P set; shapes from the plan) */
+static cudaError_t launch_x2(const TmaPlan* T, TmaStepArgs A, int gi, int wi, int sms, cudaStream_t st) {
+  const StepParams& P = A.P;
+  const DirDev& x = P.s;
+  const DirDev& y = P.o;
+  A.EG = T->EG2;
+  A.hw = T->hw2;
+  const int BW = A.EG * P.lay.Q;
+  const int gb = (P.mode != ST_CORR) ? KR * BW * 8 : 0;
+  const int wb = (P.mode != ST_NONE) ? KR * BW * 8 : 0;
+  const int hb = (P.mode != ST_NONE) ? KR * A.hw * 8 : 0;
+  // [G lo | G hi | W lo | W hi | H lo | H hi]; each upper box 128 bytes off the lower one modulo 256
+  auto hi_off = [](int bytes) {
+    int o = (bytes + 127) & ~127;
+    if (o % 256 == 0) o += 128;
+    return o;
+  };
+  A.hi_g = hi_off(gb);
+  A.hi_w = hi_off(wb);
+  A.hi_h = hi_off(hb);
+  A.off_w = gb ? (A.hi_g + gb + 255) & ~255 : 0;
+  A.off_h = A.off_w + (wb ? (A.hi_w + wb + 255) & ~255 : 0);
+  A.stage_bytes = (A.off_h + (hb ? A.hi_h + hb : 0) + 255) & ~255;
+  A.tx_bytes = 2 * (gb + wb + hb);
+  A.fac_doubles = (P.f.cfs + 15) & ~15;
+  A.wb_doubles = P.wtab ? A.EG * 5 * P.lay.Q : 0;
+  A.S = XH / KR;
+  const int budget = SMEM_OPTIN - 4096;
+  A.nstages = (budget - 2 * A.fac_doubles * 8 - 2 * A.wb_doubles * 8) / A.stage_bytes;
+  if (A.nstages > P.tun.nst[0]) A.nstages = P.tun.nst[0];
+  if (A.nstages > A.S) A.nstages = A.S;
+  if (A.nstages < 1) A.nstages = 1;
+  A.fac_off = A.nstages * A.stage_bytes;
+  A.wb_off = A.fac_off + 2 * A.fac_doubles * 8;
+  A.bar_off = A.wb_off + 2 * A.wb_doubles * 8;
+  const int ngroups = (y.n + A.EG - 1) / A.EG;
+  A.ntiles = ngroups * x.n * 2;
+  A.fS = make_fdiv(A.S);
+  A.fN = make_fdiv(A.nstages);
+  A.fG = make_fdiv(ngroups);
+  A.fT = make_fdiv(x.n);
+  const size_t smem = (size_t)A.bar_off + 2 * A.nstages * sizeof(uint64_t);
+  const int grid = A.ntiles < sms ? A.ntiles : sms;
+  const CUtensorMap* g = T->xv2[gi];
+  const CUtensorMap* w = T->xv2[wi];
+  switch (P.mode) {
+    case ST_NONE: return launch_x2_mode<ST_NONE>(A, g, w, grid, smem, st);
+    case ST_APPLY: return launch_x2_mode<ST_APPLY>(A, g, w, grid, smem, st);
+    default: return launch_x2_mode<ST_CORR>(A, g, w, grid, smem, st);
+  }
+}
+
 /* Launch the bubble-line part of one half-step.  ia_g / ia_w: indices of the
  * G and Xp arrays among (Gp, X1, X2) (-1 when unused). */
 cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int ia_w, cudaStream_t st,
@@ -1013,6 +1312,7 @@ cudaError_t tma_launch_step(const TmaPlan* T, const StepParams& P, int ia_g, int
     const size_t smem = (size_t)A.bar_off + 2 * A.nstages * sizeof(uint64_t);
     const int grid = A.ntiles < sms ? A.ntiles : sms;
     const int cl = chain_len(x.p, 0);
+    if (cl > XH && T->x2ok && !P.tun.no_x2) return launch_x2(T, A, gi, wi, sms, st);
     const CUtensorMap* g = T->xv[gi];
     const CUtensorMap* w = T->xv[wi];
     switch (P.mode) {

@@ -62,6 +62,11 @@ SMALL = [
     # (reading R23) with the x kernel's 128-position chains (spilled half)
     (rmesh(4, 0, 1, 41), 20, rmesh(3, 0, 1, 42), 200, 1.0, 0, 1e-10),  # 19
     (rmesh(3, 0, 2, 43), 32, rmesh(2, 0, 1, 44), 256, 0.5, 1, 1e-10),   # config-4 degrees, Neumann
+    # long x chains natively (no transpose): the two-threads-per-chain x kernel;
+    # p = 130: the odd chain has exactly 64 positions (empty upper half), the
+    # even one 65; p = 181: ragged halves, several column tiles (Q = 24)
+    (rmesh(2, 0, 1, 45), 130, rmesh(7, 0, 1, 46), 18, 1.0, 1, 1e-10),   # 21
+    (rmesh(3, 0, 1, 47), 181, rmesh(11, 0, 2, 48), 25, 0.0, 0, 1e-10),  # 22
 ]
 MIXED = list(range(12, 17))
 CONFIG5_SHAPE = [17, 18]
