@@ -57,10 +57,12 @@ struct FacView {
 
 /* Chains longer than 64 positions (p > 129) get tables over 128 positions and
  * the spike coefficients of the two-threads-per-chain x half-step (tma_step.cu,
- * k_xstep_tma2) behind them, at cf + fac_spk_off: for c < 64 the influence
- * beta_c of the value entering the lower half on y_c (beta_63 = -hd_63,
- * beta_c = -hd_c beta_{c+1}), for c >= 64 the influence gamma_c of z_63 on z_c
- * (gamma_64 = -hu_64, gamma_c = -hu_c gamma_{c-1}). */
+ * k_xstep_tma2) behind them, at cf + fac_spk_off.  A half swept with entry 0
+ * differs from the true sweep by the entry times a fixed vector: for c < 64,
+ * zeta_c = (L^{-1} beta)_c with beta_63 = -hd_63, beta_c = -hd_c beta_{c+1} (the
+ * influence of y_64 on z_c through y_c = a_c + beta_c y_64); for c >= 64,
+ * gamma_c with gamma_64 = -hu_64, gamma_c = -hu_c gamma_{c-1} (the influence of
+ * z_63 on z_c). */
 HD int fac_cf_pos(const DirDev& d) { return d.p / 2 > 64 ? 128 : (d.p / 2 + 7) & ~7; }
 HD int fac_spk_off(const DirDev& d) { return 4 * fac_cf_pos(d) + 2; }
 HD int fac_cfs(const DirDev& d) { return fac_spk_off(d) + (d.p / 2 > 64 ? 128 : 0); }

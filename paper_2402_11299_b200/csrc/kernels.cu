@@ -114,6 +114,11 @@ __global__ void k_factor_chains(DirDev d, const double* __restrict__ kap, const 
         bt = c < m ? -cf[4 * c + 1] * bt : 0.0;
         spk[c] = bt;
       }
+      double zt = 0.0;  // zeta = L^{-1} beta (lower half): the entry's influence on z_c
+      for (int c = 0; c < 64; ++c) {
+        zt = fma(-cf[4 * c + 2], zt, cf[4 * c] * spk[c]);
+        spk[c] = zt;
+      }
       double gm = 1.0;
       for (int c = 64; c < 128; ++c) {
         gm = c < m ? -cf[4 * c + 2] * gm : 0.0;

@@ -448,8 +448,7 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma(const TmaStepArgs A, const 
 /* with entry 0 and the true entry (one shuffle at the end of the       */
 /* sweep) is added through the tabled influence coefficients (spike     */
 /* coefficients, hpfem_internal.h fac_spk_off):                         */
-/*   down: y_c = a_c + beta_c y_64  (c < 64),                           */
-/*   up:   z_c = u_c + gamma_c z_63 (c >= 64).                          */
+/*   z_c = u_c + zeta_c y_64  (c < 64),  z_c = u_c + gamma_c z_63 (c >= 64) */
 /* Both half-warps run the same instructions (the entry is 0 where it   */
 /* does not apply).  Same factors, same right-hand sides; the           */
 /* association of the products differs from the sequential sweep        */
@@ -612,42 +611,42 @@ __global__ void __launch_bounds__(NT, 1) k_xstep_tma2(const TmaStepArgs A, const
         ys[c] = yv;
       }
     }
-    // the value entering the lower half: y_64 of the upper half (0 for the upper half itself)
+    // Each half has swept down with entry 0.  The true lower half is
+    // y_c = a_c + beta_c y_64, so its up sweep is u_c + zeta_c y_64 with
+    // zeta = L^{-1} beta tabled; the true upper half of the up sweep is
+    // u_c + gamma_c z_63.  Both halves: one up sweep with entry 0, then one
+    // tabled correction, z_c = u_c + t_c e (e = y_64 below, z_63 above).
     const double y64 = __shfl_sync(0xffffffffu, yv, (lane & 15) + 16);
-    const double e1 = h ? 0.0 : y64;
-    // up sweep of both halves, entry 0, on y_c = a_c + beta_c y_64
+    constexpr int UB = 8;
     double z = 0.0;
 #pragma unroll
-    for (int c0 = 0; c0 < XH; c0 += KR) {
-      double2 fz[KR];
-      double sv[KR];
+    for (int c0 = 0; c0 < XH; c0 += UB) {
+      double2 fz[UB];
 #pragma unroll
-      for (int u = 0; u < KR; ++u) {
-        fz[u] = *reinterpret_cast<const double2*>(fbh + 4 * (c0 + u) + 2);  // (hu, il)
-        sv[u] = sp[c0 + u];
-      }
+      for (int u = 0; u < UB; ++u) fz[u] = *reinterpret_cast<const double2*>(fbh + 4 * (c0 + u) + 2);  // (hu, il)
 #pragma unroll
-      for (int u = 0; u < KR; ++u) {
+      for (int u = 0; u < UB; ++u) {
         const int c = c0 + u;
-        z = fma(-fz[u].x, z, fz[u].y * fma(sv[u], e1, ys[c]));
+        z = fma(-fz[u].x, z, fz[u].y * ys[c]);
         ys[c] = z;
       }
     }
-    // the value entering the upper half: z_63 of the lower half
-    const double z63 = __shfl_sync(0xffffffffu, z, lane & 15);
-    const double e2 = h ? z63 : 0.0;
+    const double z63 = __shfl_sync(0xffffffffu, fma(sp[XH - 1], y64, z), lane & 15);  // (lower lanes: the true z_63)
+    const double e2 = h ? z63 : y64;
     if (valid) {
-      double* __restrict__ out = P.out + P.lay.hb + (size_t)ey * Q + ky;
+      // row of chain position c: x.nh + (pi + 2 c) x.n + e_x, i.e. a fixed stride from the half's first row
+      double* __restrict__ op =
+          P.out + P.lay.hb + (size_t)ey * Q + ky + (size_t)(x.nh + (pi + 2 * cb) * x.n + e_x) * P.ld;
+      const size_t rs = (size_t)2 * x.n * P.ld;
+      const int mh = m - cb;  // positions of this half inside the chain
 #pragma unroll
-      for (int c0 = 0; c0 < XH; c0 += KR) {
-        double sv[KR];
+      for (int c0 = 0; c0 < XH; c0 += UB) {
+        double sv[UB];
 #pragma unroll
-        for (int u = 0; u < KR; ++u) sv[u] = sp[c0 + u];
+        for (int u = 0; u < UB; ++u) sv[u] = sp[c0 + u];
 #pragma unroll
-        for (int u = 0; u < KR; ++u) {
-          const int c = cb + c0 + u;
-          if (c < m) out[(size_t)(x.nh + (pi + 2 * c) * x.n + e_x) * P.ld] = fma(sv[u], e2, ys[c0 + u]);
-        }
+        for (int u = 0; u < UB; ++u)
+          if (c0 + u < mh) op[(size_t)(c0 + u) * rs] = fma(sv[u], e2, ys[c0 + u]);
       }
     }
   }

@@ -14,7 +14,7 @@ seen_fn = 0
 for r in rows:
     if not r:
         continue
-    if r[0] == "Function Name":
+    if r[0] == "Kernel Name":
         seen_fn += 1
         if seen_fn > 1:
             break  # first launch only
