@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "small_cases or stress or (config_full and (2 or 4))" 2>&1 | tail -2
+bash scripts/ab_cmp.sh 5 1
+bash scripts/ab_cmp.sh 3 1
