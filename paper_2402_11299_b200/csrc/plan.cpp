@@ -762,7 +762,10 @@ int run_step(hpfem_plan_t pl, const Workspace& w, StepParams P, cudaStream_t st,
     // The hat Schur solves of those hat lines follow them on the side stream;
     // the ones of the bubble lines need the bubble kernel only, so neither
     // waits for the other (joined before the next half-step).
-    const bool split = P.s.nh > 0 && hats_split_ok(P) && !pl->tun.no_hat_split;
+    // (not for the stream slots of hpfem_solve_batched: their solves are
+    // launch-bound and the extra launch costs more than the overlap gains --
+    // config 2, B = 256: 220 -> 350 ms)
+    const bool split = P.s.nh > 0 && hats_split_ok(P) && !pl->tun.no_hat_split && &w == &pl->ws;
     if (split) {
       StepParams K = P;
       K.hl_begin = P.dir == 1 ? P.o.nb : 0;

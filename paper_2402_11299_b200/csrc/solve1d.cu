@@ -86,20 +86,24 @@ __device__ double enter_up(Aff f, double* sa, double* sb) {
 
 }  // namespace
 
-/* One CTA per right-hand side at a time (grid-stride over them).  Passes
- * over the row: F read once; U written with the down-sweep values y, read
- * back and overwritten with the final x_b in the up sweep, into which the
- * bubble correction x_b = z_b - v_L x_hL - v_R x_hR is fused (the hat
+/* One CTA takes RB right-hand sides at a time (grid-stride over groups of
+ * RB).  Passes over a row: F read once; U written with the down-sweep values
+ * y, read back and overwritten with the final x_b in the up sweep, into which
+ * the bubble correction x_b = z_b - v_L x_hL - v_R x_hR is fused (the hat
  * solution is known by then: the hat right-hand side needs only the
  * chain-first z_0 = il_0 y_0, available right after the down sweep).
- * Chain loads are batched CB positions ahead of the dependent FMAs.
- * hats_in_smem: the hat values live in shared memory [nh] (else in the hat
- * slots of the output row, same code with global addresses). */
+ * A thread sweeps the SAME chain of all RB right-hand sides together: the
+ * chain factors (il, g, v_L, v_R -- 6 of the 8 loads per dof of a single
+ * right-hand side) are loaded once per RB rows, and the RB recurrences are
+ * independent (ILP).  Chain loads are batched CB positions ahead of the
+ * dependent FMAs.  hats_in_smem: the hat values live in shared memory
+ * [RB][nh] (else in the hat slots of the output rows, same code with global
+ * addresses). */
 constexpr int CB = 4;   // chain positions per load batch (down sweeps)
 constexpr int CBU = 4;  // the same for the up sweeps
-constexpr int NCH = 1;  // chains per thread in flight (loads of all of them batched together)
 constexpr int HU = 8;   // hats per load batch in the block sweeps
 
+template <int RB>
 __global__ void __launch_bounds__(NT1) k_solve1d(DirDev d, FacView f, int nrhs, int hats_in_smem,
                                                     const double* __restrict__ F, double* __restrict__ U) {
   extern __shared__ double sh[];
@@ -114,205 +118,232 @@ __global__ void __launch_bounds__(NT1) k_solve1d(DirDev d, FacView f, int nrhs, 
   const int HB = (nh + NT1 - 1) / NT1;  // hats per thread (contiguous block)
   const int ta = threadIdx.x * HB, tb = min(nh, ta + HB);
   const int m0 = chain_len(d.p, 0);     // the longer (even) chain
-  for (int rhs = blockIdx.x; rhs < nrhs; rhs += gridDim.x) {
-    const double* __restrict__ Fr = F + (size_t)rhs * d.N;
-    double* __restrict__ Ur = U + (size_t)rhs * d.N;
-    double* H = hats_in_smem ? sh : Ur;  // hat values r -> y -> x
+  for (int rhs0 = blockIdx.x * RB; rhs0 < nrhs; rhs0 += gridDim.x * RB) {
+    const double* Fr[RB];
+    double* Ur[RB];
+    double* H[RB];  // hat values r -> y -> x
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int rhs = min(rhs0 + r, nrhs - 1);  // a ragged last group repeats its last row (same values rewritten)
+      Fr[r] = F + (size_t)rhs * d.N;
+      Ur[r] = U + (size_t)rhs * d.N;
+      H[r] = hats_in_smem ? sh + (size_t)r * nh : Ur[r];
+    }
     // 1. down sweeps L^T y = f of every chain (consecutive threads:
     //    consecutive elements, coalesced); y parked in the output row, the
     //    chain-first slot gets z_0 = il_0 y_0 (the first up-sweep step)
-    for (int ch0 = threadIdx.x; ch0 < 2 * n; ch0 += NT1 * NCH) {
-      double y[NCH];
-      int pe[NCH], mm[NCH];
+    for (int ch = threadIdx.x; ch < 2 * n; ch += NT1) {
+      const int pi = ch < n ? 0 : 1, e = ch - pi * n;
+      const int mm = chain_len(d.p, pi);
+      const int pe = pi * n + e;  // b of position c: pe + 2 c n
+      double y[RB];
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        const int ch = ch0 + j * NT1;
-        const int pi = ch < n ? 0 : 1, e = ch - pi * n;
-        mm[j] = ch < 2 * n ? chain_len(d.p, pi) : 0;
-        pe[j] = pi * n + e;  // b of position c: pe + 2 c n
-        y[j] = 0.0;
-      }
+      for (int r = 0; r < RB; ++r) y[r] = 0.0;
       for (int c0 = m0 - 1; c0 >= 0; c0 -= CB) {
-        double fv[NCH][CB], gv[NCH][CB], lv[NCH][CB];
+        double fv[RB][CB], gv[CB], lv[CB];
 #pragma unroll
-        for (int j = 0; j < NCH; ++j)
+        for (int u = 0; u < CB; ++u) {
+          const int c = c0 - u;
+          const bool ok = c >= 0 && c < mm;
+          const int b = pe + 2 * (ok ? c : 0) * n;
+          gv[u] = ok ? g[b] : 0.0;
+          lv[u] = ok ? il[b] : 0.0;
 #pragma unroll
-          for (int u = 0; u < CB; ++u) {
-            const int c = c0 - u;
-            const bool ok = c >= 0 && c < mm[j];
-            const int b = pe[j] + 2 * (ok ? c : 0) * n;
-            fv[j][u] = ok ? Fr[nh + b] : 0.0;
-            gv[j][u] = ok ? g[b] : 0.0;
-            lv[j][u] = ok ? il[b] : 0.0;
-          }
+          for (int r = 0; r < RB; ++r) fv[r][u] = ok ? Fr[r][nh + b] : 0.0;
+        }
 #pragma unroll
-        for (int j = 0; j < NCH; ++j)
+        for (int u = 0; u < CB; ++u) {
+          const int c = c0 - u;
+          if (c >= 0 && c < mm) {
 #pragma unroll
-          for (int u = 0; u < CB; ++u) {
-            const int c = c0 - u;
-            if (c >= 0 && c < mm[j]) {
-              y[j] = (fv[j][u] - gv[j][u] * y[j]) * lv[j][u];
-              Ur[nh + pe[j] + 2 * c * n] = c == 0 ? y[j] * lv[j][u] : y[j];
+            for (int r = 0; r < RB; ++r) {
+              y[r] = (fv[r][u] - gv[u] * y[r]) * lv[u];
+              Ur[r][nh + pe + 2 * c * n] = c == 0 ? y[r] * lv[u] : y[r];
             }
           }
+        }
       }
     }
     __syncthreads();
-    // 2. hat right-hand sides r_h = f_h - B z
-#pragma unroll 4
+    // 2. hat right-hand sides r_h = f_h - B z (coupling coefficients once per hat for the RB rows)
+#pragma unroll 2
     for (int t = threadIdx.x; t < nh; t += NT1) {
       const int node = node_of_hat(t, d.bc), eL = node - 1, eR = node;
-      double r = Fr[t];
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
       if (eL >= 0) {
         const double dl = d.delta[eL];
-        r -= s_hat_bub(S, dl, 1, 0) * Ur[nh + eL];
-        if (k1) r -= s_hat_bub(S, dl, 1, 1) * Ur[nh + n + eL];
+        c0 = s_hat_bub(S, dl, 1, 0);
+        if (k1) c1 = s_hat_bub(S, dl, 1, 1);
       }
       if (eR <= n - 1) {
         const double dr = d.delta[eR];
-        r -= s_hat_bub(S, dr, 0, 0) * Ur[nh + eR];
-        if (k1) r -= s_hat_bub(S, dr, 0, 1) * Ur[nh + n + eR];
+        c2 = s_hat_bub(S, dr, 0, 0);
+        if (k1) c3 = s_hat_bub(S, dr, 0, 1);
       }
-      H[t] = r;
+      const int iL = nh + max(eL, 0), iR = nh + min(eR, n - 1);  // absent elements: zero coefficients
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        double rr = Fr[r][t];
+        rr -= c0 * Ur[r][iL];
+        if (k1) rr -= c1 * Ur[r][n + iL];
+        rr -= c2 * Ur[r][iR];
+        if (k1) rr -= c3 * Ur[r][n + iR];
+        H[r][t] = rr;
+      }
     }
     __syncthreads();
     // 3. hat Schur solve: y_t = il_t r_t - (g_t il_t) y_{t+1} (t descending),
     //    then x_t = il_t y_t - (g_{t-1} il_t) x_{t-1} (t ascending), each as
-    //    block maps + scan + local sweep; loads HU hats ahead
+    //    block maps + scan + local sweep; loads HU hats ahead, the factors
+    //    once for the RB rows
     if (nh > 0) {
-      Aff fm{0.0, 1.0};
+      Aff fm[RB];
+      double v[RB];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) fm[r] = Aff{0.0, 1.0};
       for (int t0 = tb - 1; t0 >= ta; t0 -= HU) {
-        double hv[HU], lv[HU], gv[HU];
+        double hv[RB][HU], lv[HU], hd[HU];
 #pragma unroll
         for (int u = 0; u < HU; ++u) {
           const int t = t0 - u >= ta ? t0 - u : ta;
-          hv[u] = H[t];
           lv[u] = ilh[t];
-          gv[u] = gh[t];
+          hd[u] = gh[t] * lv[u];
+#pragma unroll
+          for (int r = 0; r < RB; ++r) hv[r][u] = H[r][t];
         }
 #pragma unroll
         for (int u = 0; u < HU; ++u)
           if (t0 - u >= ta) {
-            const double hd = gv[u] * lv[u];
-            fm = Aff{fma(-hd, fm.a, lv[u] * hv[u]), -hd * fm.b};
+#pragma unroll
+            for (int r = 0; r < RB; ++r) fm[r] = Aff{fma(-hd[u], fm[r].a, lv[u] * hv[r][u]), -hd[u] * fm[r].b};
           }
       }
-      double v = enter_down(fm, sa, sb);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) v[r] = enter_down(fm[r], sa, sb);
       for (int t0 = tb - 1; t0 >= ta; t0 -= HU) {
-        double hv[HU], lv[HU], gv[HU];
+        double hv[RB][HU], lv[HU], hd[HU];
 #pragma unroll
         for (int u = 0; u < HU; ++u) {
           const int t = t0 - u >= ta ? t0 - u : ta;
-          hv[u] = H[t];
           lv[u] = ilh[t];
-          gv[u] = gh[t];
+          hd[u] = gh[t] * lv[u];
+#pragma unroll
+          for (int r = 0; r < RB; ++r) hv[r][u] = H[r][t];
         }
 #pragma unroll
         for (int u = 0; u < HU; ++u)
           if (t0 - u >= ta) {
-            v = fma(-(gv[u] * lv[u]), v, lv[u] * hv[u]);
-            H[t0 - u] = v;
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+              v[r] = fma(-hd[u], v[r], lv[u] * hv[r][u]);
+              H[r][t0 - u] = v[r];
+            }
           }
       }
-      fm = Aff{0.0, 1.0};
+#pragma unroll
+      for (int r = 0; r < RB; ++r) fm[r] = Aff{0.0, 1.0};
       for (int t0 = ta; t0 < tb; t0 += HU) {
-        double hv[HU], lv[HU], gv[HU];
+        double hv[RB][HU], lv[HU], hu[HU];
 #pragma unroll
         for (int u = 0; u < HU; ++u) {
           const int t = t0 + u < tb ? t0 + u : tb - 1;
-          hv[u] = H[t];
           lv[u] = ilh[t];
-          gv[u] = t > 0 ? gh[t - 1] : 0.0;
+          hu[u] = (t > 0 ? gh[t - 1] : 0.0) * lv[u];
+#pragma unroll
+          for (int r = 0; r < RB; ++r) hv[r][u] = H[r][t];
         }
 #pragma unroll
         for (int u = 0; u < HU; ++u)
           if (t0 + u < tb) {
-            const double hu = gv[u] * lv[u];
-            fm = Aff{fma(-hu, fm.a, lv[u] * hv[u]), -hu * fm.b};
+#pragma unroll
+            for (int r = 0; r < RB; ++r) fm[r] = Aff{fma(-hu[u], fm[r].a, lv[u] * hv[r][u]), -hu[u] * fm[r].b};
           }
       }
-      v = enter_up(fm, sa, sb);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) v[r] = enter_up(fm[r], sa, sb);
       for (int t0 = ta; t0 < tb; t0 += HU) {
-        double hv[HU], lv[HU], gv[HU];
+        double hv[RB][HU], lv[HU], hu[HU];
 #pragma unroll
         for (int u = 0; u < HU; ++u) {
           const int t = t0 + u < tb ? t0 + u : tb - 1;
-          hv[u] = H[t];
           lv[u] = ilh[t];
-          gv[u] = t > 0 ? gh[t - 1] : 0.0;
+          hu[u] = (t > 0 ? gh[t - 1] : 0.0) * lv[u];
+#pragma unroll
+          for (int r = 0; r < RB; ++r) hv[r][u] = H[r][t];
         }
 #pragma unroll
         for (int u = 0; u < HU; ++u)
           if (t0 + u < tb) {
-            v = fma(-(gv[u] * lv[u]), v, lv[u] * hv[u]);
-            H[t0 + u] = v;
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+              v[r] = fma(-hu[u], v[r], lv[u] * hv[r][u]);
+              H[r][t0 + u] = v[r];
+            }
           }
       }
       __syncthreads();
       if (hats_in_smem)
-        for (int t = threadIdx.x; t < nh; t += NT1) Ur[t] = H[t];
+        for (int t = threadIdx.x; t < nh; t += NT1) {
+#pragma unroll
+          for (int r = 0; r < RB; ++r) Ur[r][t] = H[r][t];
+        }
     }
     // 4. up sweeps L z = y with the bubble correction fused:
     //    x_c = z_c - v_L x_hL - v_R x_hR, written once
-    for (int ch0 = threadIdx.x; ch0 < 2 * n; ch0 += NT1 * NCH) {
-      double z[NCH], gp[NCH], xl[NCH], xr[NCH];
-      int pe[NCH], mm[NCH];
+    for (int ch = threadIdx.x; ch < 2 * n; ch += NT1) {
+      const int pi = ch < n ? 0 : 1, e = ch - pi * n;
+      const int mm = chain_len(d.p, pi);
+      const int pe = pi * n + e;
+      const int hlt = hat_of_node(e, n, d.bc), hrt = hat_of_node(e + 1, n, d.bc);
+      const bool hl = hlt >= 0, hr = hrt >= 0;
+      double z[RB], xl[RB], xr[RB];
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        const int ch = ch0 + j * NT1;
-        const int pi = ch < n ? 0 : 1, e = ch - pi * n;
-        mm[j] = ch < 2 * n ? chain_len(d.p, pi) : 0;
-        pe[j] = pi * n + e;
-        const int hl = hat_of_node(e, n, d.bc), hr = hat_of_node(e + 1, n, d.bc);
-        xl[j] = (mm[j] > 0 && hl >= 0) ? H[hl] : 0.0;  // 0: the term is skipped below
-        xr[j] = (mm[j] > 0 && hr >= 0) ? H[hr] : 0.0;
-        z[j] = 0.0;
-        gp[j] = 0.0;
+      for (int r = 0; r < RB; ++r) {
+        xl[r] = (mm > 0 && hl) ? H[r][hlt] : 0.0;  // 0: the term is skipped below
+        xr[r] = (mm > 0 && hr) ? H[r][hrt] : 0.0;
+        z[r] = 0.0;
       }
+      double gp = 0.0;
       for (int c0 = 0; c0 < m0; c0 += CBU) {
-        double yv[NCH][CBU], gv[NCH][CBU], lv[NCH][CBU], vl[NCH][CBU], vr[NCH][CBU];
+        double yv[RB][CBU], gv[CBU], lv[CBU], vl[CBU], vr[CBU];
 #pragma unroll
-        for (int j = 0; j < NCH; ++j)
+        for (int u = 0; u < CBU; ++u) {
+          const int c = c0 + u;
+          const bool ok = c < mm;
+          const int b = pe + 2 * (ok ? c : 0) * n;
+          gv[u] = ok ? g[b] : 0.0;
+          lv[u] = ok ? il[b] : 0.0;
+          vl[u] = ok ? f.vL[b] : 0.0;
+          vr[u] = ok ? f.vR[b] : 0.0;
 #pragma unroll
-          for (int u = 0; u < CBU; ++u) {
-            const int c = c0 + u;
-            const bool ok = c < mm[j];
-            const int b = pe[j] + 2 * (ok ? c : 0) * n;
-            yv[j][u] = ok ? Ur[nh + b] : 0.0;
-            gv[j][u] = ok ? g[b] : 0.0;
-            lv[j][u] = ok ? il[b] : 0.0;
-            vl[j][u] = ok ? f.vL[b] : 0.0;
-            vr[j][u] = ok ? f.vR[b] : 0.0;
-          }
+          for (int r = 0; r < RB; ++r) yv[r][u] = ok ? Ur[r][nh + b] : 0.0;
+        }
 #pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-          const int ch = ch0 + j * NT1;
-          const int e = ch < n ? ch : ch - n;
-          const bool hl = hat_of_node(e, n, d.bc) >= 0, hr = hat_of_node(e + 1, n, d.bc) >= 0;
+        for (int u = 0; u < CBU; ++u) {
+          const int c = c0 + u;
+          if (c < mm) {
 #pragma unroll
-          for (int u = 0; u < CBU; ++u) {
-            const int c = c0 + u;
-            if (c < mm[j]) {
-              z[j] = c == 0 ? yv[j][u] : (yv[j][u] - gp[j] * z[j]) * lv[j][u];  // slot 0 holds z_0
-              gp[j] = gv[j][u];
-              double x = z[j];
-              if (hl) x -= vl[j][u] * xl[j];
-              if (hr) x -= vr[j][u] * xr[j];
-              Ur[nh + pe[j] + 2 * c * n] = x;
+            for (int r = 0; r < RB; ++r) {
+              z[r] = c == 0 ? yv[r][u] : (yv[r][u] - gp * z[r]) * lv[u];  // slot 0 holds z_0
+              double x = z[r];
+              if (hl) x -= vl[u] * xl[r];
+              if (hr) x -= vr[u] * xr[r];
+              Ur[r][nh + pe + 2 * c * n] = x;
             }
+            gp = gv[u];
           }
         }
       }
     }
-    __syncthreads();  // H (shared) is rewritten by the next right-hand side
+    __syncthreads();  // H (shared) is rewritten by the next group
   }
 }
 
-cudaError_t launch_solve1d(const DirDev& d, const FacView& f, int nrhs, const double* F, double* U,
-                           cudaStream_t st) {
-  if (nrhs <= 0) return cudaSuccess;
+template <int RB>
+static cudaError_t launch_solve1d_rb(const DirDev& d, const FacView& f, int nrhs, const double* F, double* U,
+                                     cudaStream_t st) {
   // hats in shared memory when they are few enough not to limit occupancy
-  const size_t hb = sizeof(double) * (size_t)d.nh;
+  const size_t hb = sizeof(double) * (size_t)d.nh * RB;
   const int in_smem = hb <= 48 * 1024 ? 1 : 0;
   const size_t smem = in_smem ? hb : 0;
   int dev = 0, sms = 148;
@@ -320,9 +351,23 @@ cudaError_t launch_solve1d(const DirDev& d, const FacView& f, int nrhs, const do
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // one wave of up to 8 resident CTAs per SM, grid-stride over the rest
   long long g = 8LL * sms;
-  if (g > nrhs) g = nrhs;
-  k_solve1d<<<(unsigned)g, NT1, smem, st>>>(d, f, nrhs, in_smem, F, U);
+  const long long groups = (nrhs + RB - 1) / RB;
+  if (g > groups) g = groups;
+  k_solve1d<RB><<<(unsigned)g, NT1, smem, st>>>(d, f, nrhs, in_smem, F, U);
   return cudaGetLastError();
+}
+
+cudaError_t launch_solve1d(const DirDev& d, const FacView& f, int nrhs, const double* F, double* U,
+                           cudaStream_t st) {
+  if (nrhs <= 0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // two rows per CTA once there are enough rows to fill the SMs twice over
+  // (measured at 1024 rows, N = 65535: 1 / 2 / 4 rows per CTA 0.578 / 0.498 /
+  // 0.531 ms at p = 256, 1.97 / 1.63 / 1.80 ms at p = 4)
+  if (nrhs >= 4 * sms) return launch_solve1d_rb<2>(d, f, nrhs, F, U, st);
+  return launch_solve1d_rb<1>(d, f, nrhs, F, U, st);
 }
 
 }  // namespace hpfem
