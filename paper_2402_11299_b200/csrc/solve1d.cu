@@ -24,7 +24,10 @@
  * U written); the down-sweep values make one extra round trip through the
  * output row (L2 when the rows in flight fit).
  */
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "hpfem_internal.h"
 #include "ops1d.h"
@@ -357,12 +360,355 @@ static cudaError_t launch_solve1d_rb(const DirDev& d, const FacView& f, int nrhs
   return cudaGetLastError();
 }
 
+/* ------------------------------------------------------------------ */
+/* Cluster form (round 2): one thread-block CLUSTER per right-hand side, */
+/* the row's down-sweep values held in the distributed shared memory of  */
+/* its CTAs instead of making a round trip through the output row -- F   */
+/* is read once and U written once (the 16 algorithmic bytes per dof;    */
+/* the kernel above moves 32).  CTA r of the cluster owns the elements   */
+/* [r EPC, (r+1) EPC) with their chains and left nodes (the last CTA     */
+/* also node n).  The hat Schur recurrences cross the cluster as affine  */
+/* maps: block maps per thread, a CTA scan that keeps the maps (not just */
+/* their value at entry 0), the CTA totals exchanged through             */
+/* distributed shared memory -- 4 cluster barriers per right-hand side.  */
+/* Chain-first values and hat values of the neighbouring CTA (one        */
+/* element / node each) are read remotely.                               */
+/* ------------------------------------------------------------------ */
+namespace {
+
+/* exclusive suffix composition over the CTA's threads: the map from the value
+ * entering the CTA's LAST thread to the value entering this thread (down
+ * sweep, the recurrence runs from the last thread to the first); total = the
+ * whole CTA's map.  f: this thread's block map. */
+__device__ Aff suffix_maps(Aff f, double* sa, double* sb, Aff& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Aff g{__shfl_down_sync(0xffffffffu, f.a, d), __shfl_down_sync(0xffffffffu, f.b, d)};
+    if (lane + d < 32) f = after(f, g);
+  }
+  if (lane == 0) {
+    sa[w] = f.a;
+    sb[w] = f.b;
+  }
+  __syncthreads();
+  Aff C{0.0, 1.0};  // later warps: the value passes through warp nw-1 first
+  for (int u = nw - 1; u > w; --u) C = after(Aff{sa[u], sb[u]}, C);
+  Aff nx{__shfl_down_sync(0xffffffffu, f.a, 1), __shfl_down_sync(0xffffffffu, f.b, 1)};
+  if (lane == 31) nx = Aff{0.0, 1.0};
+  Aff T0{sa[0], sb[0]};
+  Aff C0{0.0, 1.0};
+  for (int u = nw - 1; u > 0; --u) C0 = after(Aff{sa[u], sb[u]}, C0);
+  total = after(T0, C0);
+  __syncthreads();  // sa / sb reused
+  return after(nx, C);
+}
+
+/* the same for a recurrence from the first thread to the last (up sweep) */
+__device__ Aff prefix_maps(Aff f, double* sa, double* sb, Aff& total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Aff g{__shfl_up_sync(0xffffffffu, f.a, d), __shfl_up_sync(0xffffffffu, f.b, d)};
+    if (lane >= d) f = after(f, g);
+  }
+  if (lane == 31) {
+    sa[w] = f.a;
+    sb[w] = f.b;
+  }
+  __syncthreads();
+  Aff C{0.0, 1.0};  // earlier warps: the value passes through warp 0 first
+  for (int u = 0; u < w; ++u) C = after(Aff{sa[u], sb[u]}, C);
+  Aff pv{__shfl_up_sync(0xffffffffu, f.a, 1), __shfl_up_sync(0xffffffffu, f.b, 1)};
+  if (lane == 0) pv = Aff{0.0, 1.0};
+  Aff Ct{0.0, 1.0};
+  for (int u = 0; u < nw; ++u) Ct = after(Aff{sa[u], sb[u]}, Ct);
+  total = Ct;
+  __syncthreads();
+  return after(pv, C);
+}
+
+__device__ __forceinline__ int hpd(int i) { return i + (i >> 3); }  // padded hat slot (conflict-free blocks)
+
+}  // namespace
+
+struct Solve1dClSmem {
+  int EPC, LC;  // elements per CTA, chains per CTA
+  size_t y, zf, hs, tot, sc, total;  // byte offsets
+};
+__host__ __device__ inline Solve1dClSmem solve1d_cl_smem(int n, int p, int cs) {
+  Solve1dClSmem m;
+  m.EPC = (n + cs - 1) / cs;
+  m.LC = 2 * m.EPC;
+  const size_t m0 = (size_t)(p / 2);
+  m.y = 0;
+  m.zf = m.y + m0 * m.LC * 8;
+  m.hs = m.zf + (size_t)2 * (m.EPC + 1) * 8;
+  m.tot = m.hs + (size_t)(m.EPC + 2 + (m.EPC + 2) / 8 + 1) * 8;
+  m.sc = m.tot + 4 * 8;
+  m.total = m.sc + 2 * 32 * 8;
+  return m;
+}
+
+__global__ void __launch_bounds__(NT1) k_solve1d_cl(DirDev d, FacView f, int nrhs, int cs, const double* __restrict__ F,
+                                                       double* __restrict__ U) {
+  extern __shared__ __align__(16) unsigned char sm1[];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = (int)cluster.block_rank();
+  const Solve1dClSmem M = solve1d_cl_smem(d.n, d.p, cs);
+  double* ysm = reinterpret_cast<double*>(sm1 + M.y);   // [c][LC]: down-sweep values (slot 0: z_0)
+  double* zf = reinterpret_cast<double*>(sm1 + M.zf);   // [2][EPC + 1]: chain-first z of elements E0-1 .. E1-1
+  double* Hs = reinterpret_cast<double*>(sm1 + M.hs);   // hat values of nodes E0 .. (padded slots)
+  double* tot = reinterpret_cast<double*>(sm1 + M.tot); // CTA total maps: down (a, b), up (a, b)
+  double* sa = reinterpret_cast<double*>(sm1 + M.sc);
+  double* sb = sa + 32;
+  const int n = d.n, nh = d.nh, dl = drop_left(d.bc);
+  const int EPC = M.EPC, LC = M.LC;
+  const int E0 = min(n, cr * EPC), E1 = min(n, E0 + EPC), ne = E1 - E0;
+  const bool own_last = ne > 0 && E1 == n;      // this CTA also owns node n
+  const int nown = ne + (own_last ? 1 : 0);     // owned nodes E0 .. E0 + nown - 1
+  const double* __restrict__ il = f.il;
+  const double* __restrict__ g = f.g;
+  const double S = f.sig;
+  const bool k1 = d.p - 2 >= 1;
+  const int m0 = chain_len(d.p, 0);
+  const int HB = (nown + NT1 - 1) / NT1;
+  const int ia = min(nown, (int)threadIdx.x * HB), ib = min(nown, ia + HB);  // this thread's nodes (local)
+  const int ncl = gridDim.x / cs;
+  for (int rhs = blockIdx.x / cs; rhs < nrhs; rhs += ncl) {
+    const double* __restrict__ Fr = F + (size_t)rhs * d.N;
+    double* __restrict__ Ur = U + (size_t)rhs * d.N;
+    // 1. down sweeps of the owned chains into shared memory (slot 0: z_0 = il_0 y_0).
+    //    (Staging the slice of F through shared memory first and sweeping in
+    //    place, so that every DRAM load is in flight at once, measured slower:
+    //    single row 19 -> 31 us at N = 65535, p = 64.)
+    for (int lc = threadIdx.x; lc < 2 * ne; lc += NT1) {
+      const int pi = lc < ne ? 0 : 1, el = lc - pi * ne, e = E0 + el;
+      const int mm = chain_len(d.p, pi);
+      const int pe = pi * n + e;
+      const int col = pi * EPC + el;
+      double y = 0.0;
+      for (int c0 = m0 - 1; c0 >= 0; c0 -= CB) {
+        double fv[CB], gv[CB], lv[CB];
+#pragma unroll
+        for (int u = 0; u < CB; ++u) {
+          const int c = c0 - u;
+          const bool ok = c >= 0 && c < mm;
+          const int b = pe + 2 * (ok ? c : 0) * n;
+          fv[u] = ok ? Fr[nh + b] : 0.0;
+          gv[u] = ok ? g[b] : 0.0;
+          lv[u] = ok ? il[b] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < CB; ++u) {
+          const int c = c0 - u;
+          if (c >= 0 && c < mm) {
+            y = (fv[u] - gv[u] * y) * lv[u];
+            ysm[(size_t)c * LC + col] = c == 0 ? y * lv[u] : y;
+            if (c == 0) zf[pi * (EPC + 1) + el + 1] = y * lv[u];
+          }
+        }
+      }
+      if (mm == 0) zf[pi * (EPC + 1) + el + 1] = 0.0;
+    }
+    cluster.sync();  // (1) chain-first values visible to the next CTA
+    if (threadIdx.x < 2) {  // halo: element E0 - 1 of the previous CTA
+      double v = 0.0;
+      if (cr > 0 && ne > 0) {
+        const double* rz = cluster.map_shared_rank(zf, cr - 1);
+        v = rz[threadIdx.x * (EPC + 1) + EPC];  // its last element (the previous CTA is full)
+      }
+      zf[threadIdx.x * (EPC + 1)] = v;
+    }
+    __syncthreads();
+    // 2. hat right-hand sides of the owned nodes
+    for (int i = threadIdx.x; i < nown; i += NT1) {
+      const int node = E0 + i, t = node - dl;
+      double rr = 0.0;
+      if (t >= 0 && t < nh) {
+        rr = Fr[t];
+        const int eL = node - 1, eR = node;
+        if (eL >= 0) {
+          const double dlt = d.delta[eL];
+          rr -= s_hat_bub(S, dlt, 1, 0) * zf[i];
+          if (k1) rr -= s_hat_bub(S, dlt, 1, 1) * zf[(EPC + 1) + i];
+        }
+        if (eR <= n - 1) {
+          const double drt = d.delta[eR];
+          rr -= s_hat_bub(S, drt, 0, 0) * zf[i + 1];
+          if (k1) rr -= s_hat_bub(S, drt, 0, 1) * zf[(EPC + 1) + i + 1];
+        }
+      }
+      Hs[hpd(i)] = rr;
+    }
+    __syncthreads();
+    // 3. hat Schur solve across the cluster (dropped nodes: identity maps, value 0)
+    {
+      Aff fm{0.0, 1.0};
+      for (int i = ib - 1; i >= ia; --i) {
+        const int t = E0 + i - dl;
+        if (t >= 0 && t < nh) {
+          const double l = f.ilh[t], hd = f.gh[t] * l;
+          fm = Aff{fma(-hd, fm.a, l * Hs[hpd(i)]), -hd * fm.b};
+        }
+      }
+      Aff T;
+      const Aff Sx = suffix_maps(fm, sa, sb, T);
+      if (threadIdx.x == 0) {
+        tot[0] = T.a;
+        tot[1] = T.b;
+      }
+      cluster.sync();  // (2) CTA totals of the down sweep
+      double E = 0.0;
+      for (int r = cs - 1; r > cr; --r) {
+        const double* rt = cluster.map_shared_rank(tot, r);
+        E = fma(rt[1], E, rt[0]);
+      }
+      double v = fma(Sx.b, E, Sx.a);
+      for (int i = ib - 1; i >= ia; --i) {
+        const int t = E0 + i - dl;
+        if (t >= 0 && t < nh) {
+          const double l = f.ilh[t];
+          v = fma(-(f.gh[t] * l), v, l * Hs[hpd(i)]);
+          Hs[hpd(i)] = v;
+        }
+      }
+      fm = Aff{0.0, 1.0};
+      for (int i = ia; i < ib; ++i) {
+        const int t = E0 + i - dl;
+        if (t >= 0 && t < nh) {
+          const double l = f.ilh[t], hu = (t > 0 ? f.gh[t - 1] : 0.0) * l;
+          fm = Aff{fma(-hu, fm.a, l * Hs[hpd(i)]), -hu * fm.b};
+        }
+      }
+      const Aff Px = prefix_maps(fm, sa, sb, T);
+      if (threadIdx.x == 0) {
+        tot[2] = T.a;
+        tot[3] = T.b;
+      }
+      cluster.sync();  // (3) CTA totals of the up sweep
+      E = 0.0;
+      for (int r = 0; r < cr; ++r) {
+        const double* rt = cluster.map_shared_rank(tot, r);
+        E = fma(rt[3], E, rt[2]);
+      }
+      v = fma(Px.b, E, Px.a);
+      for (int i = ia; i < ib; ++i) {
+        const int t = E0 + i - dl;
+        if (t >= 0 && t < nh) {
+          const double l = f.ilh[t];
+          v = fma(-((t > 0 ? f.gh[t - 1] : 0.0) * l), v, l * Hs[hpd(i)]);
+          Hs[hpd(i)] = v;
+          Ur[t] = v;
+        }
+      }
+    }
+    cluster.sync();  // (4) hat values visible to the previous CTA
+    if (threadIdx.x == 0 && ne > 0 && !own_last) {  // node E1 belongs to the next CTA
+      const double* rh = cluster.map_shared_rank(Hs, cr + 1);
+      Hs[hpd(ne)] = rh[0];
+    }
+    __syncthreads();
+    // 4. up sweeps with the bubble correction fused, written once
+    for (int lc = threadIdx.x; lc < 2 * ne; lc += NT1) {
+      const int pi = lc < ne ? 0 : 1, el = lc - pi * ne, e = E0 + el;
+      const int mm = chain_len(d.p, pi);
+      const int pe = pi * n + e;
+      const int col = pi * EPC + el;
+      const bool hl = hat_of_node(e, n, d.bc) >= 0, hr = hat_of_node(e + 1, n, d.bc) >= 0;
+      const double xl = hl ? Hs[hpd(el)] : 0.0, xr = hr ? Hs[hpd(el + 1)] : 0.0;
+      double z = 0.0, gp = 0.0;
+      for (int c0 = 0; c0 < m0; c0 += CBU) {
+        double gv[CBU], lv[CBU], vl[CBU], vr[CBU];
+#pragma unroll
+        for (int u = 0; u < CBU; ++u) {
+          const int c = c0 + u;
+          const bool ok = c < mm;
+          const int b = pe + 2 * (ok ? c : 0) * n;
+          gv[u] = ok ? g[b] : 0.0;
+          lv[u] = ok ? il[b] : 0.0;
+          vl[u] = ok ? f.vL[b] : 0.0;
+          vr[u] = ok ? f.vR[b] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < CBU; ++u) {
+          const int c = c0 + u;
+          if (c < mm) {
+            const double yv = ysm[(size_t)c * LC + col];
+            z = c == 0 ? yv : (yv - gp * z) * lv[u];  // slot 0 holds z_0
+            gp = gv[u];
+            double x = z;
+            if (hl) x -= vl[u] * xl;
+            if (hr) x -= vr[u] * xr;
+            Ur[nh + pe + 2 * c * n] = x;
+          }
+        }
+      }
+    }
+    // (the next row's first cluster barrier orders its shared-memory writes
+    // after every remote read of this row)
+  }
+  cluster.sync();  // no CTA exits while a neighbour may still read its shared memory
+}
+
+/* cluster size of the cluster form (0 = not applicable): the smallest that
+ * lets three (else two, else one) CTAs share an SM */
+static int solve1d_cluster_size(const DirDev& d) {
+  for (size_t cap : {(size_t)72 * 1024, (size_t)110 * 1024, (size_t)220 * 1024})
+    for (int cs : {1, 2, 4, 8})
+      if (d.n >= cs && solve1d_cl_smem(d.n, d.p, cs).total <= cap) return cs;
+  return 0;
+}
+
+static cudaError_t launch_solve1d_cl(const DirDev& d, const FacView& f, int nrhs, int cs, const double* F, double* U,
+                                     cudaStream_t st) {
+  const size_t smem = solve1d_cl_smem(d.n, d.p, cs).total;
+  cudaError_t e = smem_optin((const void*)k_solve1d_cl, 227 * 1024);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_sm = smem <= 72 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
+  long long ncl = (long long)sms * per_sm / cs;
+  if (ncl > nrhs) ncl = nrhs;
+  if (ncl < 1) ncl = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ncl * cs));
+  cfg.blockDim = dim3(NT1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_solve1d_cl, d, f, nrhs, cs, F, U);
+}
+
 cudaError_t launch_solve1d(const DirDev& d, const FacView& f, int nrhs, const double* F, double* U,
                            cudaStream_t st) {
   if (nrhs <= 0) return cudaSuccess;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  {  // Cluster form for batches that one round of resident clusters covers (a
+     // latency kernel: single row at N = 65535 0.34 -> 0.038 ms at p = 4, 0.083
+     // -> 0.019 ms at p = 64; its 4 cluster barriers per row make it 2-3x
+     // slower than the row-per-CTA kernel at 1024 rows).  HPFEM_1D_CLUSTER=0
+     // disables it, =1 forces it for any batch (tests).
+    const char* v = std::getenv("HPFEM_1D_CLUSTER");
+    const int mode = v ? std::atoi(v) : -1;
+    const int cs = mode == 0 ? 0 : solve1d_cluster_size(d);
+    if (cs > 0) {
+      const size_t smem = solve1d_cl_smem(d.n, d.p, cs).total;
+      const int per_sm = smem <= 72 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
+      if (mode == 1 || (long long)nrhs * cs <= (long long)sms * per_sm)
+        return launch_solve1d_cl(d, f, nrhs, cs, F, U, st);
+    }
+  }
   // two rows per CTA once there are enough rows to fill the SMs twice over
   // (measured at 1024 rows, N = 65535: 1 / 2 / 4 rows per CTA 0.578 / 0.498 /
   // 0.531 ms at p = 256, 1.97 / 1.63 / 1.80 ms at p = 4)

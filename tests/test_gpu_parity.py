@@ -446,19 +446,29 @@ CASES_1D = [
     (rmesh(9, 0, 1, 31), 10, 2, 0.0),             # mixed: Dirichlet left, Neumann right
     (np.array([0.0, 1.0]), 5, 3, 0.0),            # mixed, one element: one hat
     (rmesh(40, 0, 2, 32), 3, 3, 2.0),             # mixed, Neumann left
+    # rows too long for one CTA's shared memory: clusters of 2 .. 8 CTAs (cluster form)
+    (rmesh(512, 0, 1, 33), 33, 0, 1.0),           # 9: N = 16895, cluster of 2
+    (rmesh(1031, -1, 1, 34), 64, 1, 0.7),         # 10: N = 65985, cluster of 8, ragged element split, Neumann
+    (np.linspace(-1, 1, 16385), 4, 0, 1.0),       # 11: Fig. 1's p = 4, N = 65535: 16383 hats across 8 CTAs
+    (W.graded_mesh(0, 1, 300, 0.97), 128, 2, 0.0),  # 12: graded, mixed ends, N = 38400
 ]
 
 
+@pytest.mark.parametrize("form", ["cluster", "rows"])
 @pytest.mark.parametrize("case", range(len(CASES_1D)))
-def test_solve1d_vs_oracle(case):
+def test_solve1d_vs_oracle(case, form, monkeypatch):
     """hpfem_solve1d (NEXT-2, Fig. 1 workload): (K + w^2 M)^{-1} F for a batch
-    of right-hand sides vs the oracle's Alg. 1 + Cor. 4.3 solve."""
+    of right-hand sides vs the oracle's Alg. 1 + Cor. 4.3 solve, through the
+    cluster form (the row in distributed shared memory) and through the
+    row-per-CTA kernel (HPFEM_1D_CLUSTER=0; 600 rows on the small shapes so
+    that the two-rows-per-CTA variant and its ragged last group run)."""
     import paper_2402_11299_b200 as hp
 
     torch = torch_cuda()
+    monkeypatch.setenv("HPFEM_1D_CLUSTER", "0" if form == "rows" else "1")
     xs, p, bc, om = CASES_1D[case]
     pl = hp.Plan1D(xs, p, bc, om)
-    nrhs = 5
+    nrhs = 5 if (form == "cluster" or pl.N > 5000) else 601
     F = np.random.default_rng(case).standard_normal((nrhs, pl.N))
     Fd = torch.from_numpy(F).cuda()
     Ud = torch.empty_like(Fd)
@@ -467,8 +477,10 @@ def test_solve1d_vs_oracle(case):
     U = Ud.cpu().numpy()
     Uref = oracle.solve1d(xs, p, bc, 1.0, om * om, F)
     err = np.linalg.norm(U - Uref) / np.linalg.norm(Uref)
-    print(f"1d case {case}: N={pl.N} rel err {err:.2e}")
-    assert err <= 1e-11
+    print(f"1d case {case} [{form}]: N={pl.N} rel err {err:.2e}")
+    # north_star's 1e-10; the small shapes sit at 1e-13 .. 1e-12, the 16383-hat
+    # Schur system of case 11 (kappa ~ n^2) at 2e-11 .. 4e-11 in either form
+    assert err <= (1e-11 if pl.N < 5000 else 1e-10)
     pl.close()
 
 
