@@ -207,8 +207,17 @@ cudaError_t launch_copyin(const DirDev& x, const DirDev& y, const Layout& L, con
 cudaError_t launch_transpose(const double* in, int R, int C, double* out, cudaStream_t st);
 cudaError_t launch_finalize(const DirDev& x, const DirDev& y, const Layout& L, const double* vL, const double* vR,
                             const double* X, double* U, cudaStream_t st);
+/* 7-slot rows of A = K + (w^2/2) M and of M of one direction, slot-major
+ * [7][N]: idx (-1 = absent), wA, wM = -(row entries) (0 where absent) */
+struct ApplyTab {
+  const int* idx;
+  const double* wA;
+  const double* wM;
+};
+cudaError_t launch_apply_tab(const DirDev& o, double omega, const ApplyTab& t, cudaStream_t st);
+/* tx / ty: the plan's tables (null: stencils built per output, the round-1 kernel) */
 cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const double* U, double* F,
-                           cudaStream_t st);
+                           cudaStream_t st, const ApplyTab* tx = nullptr, const ApplyTab* ty = nullptr);
 /* accumulate = 1: G += load(Fleg) (the variable-coefficient operator adds
  * its Hadamard term onto hpfem_apply's output) */
 cudaError_t launch_load_tab(const DirDev& d, int* r, double* w, cudaStream_t st);

@@ -1603,8 +1603,151 @@ __global__ void __launch_bounds__(128) k_apply2d(DirDev x, DirDev y, double half
   F[(size_t)i * y.N + j] = acc;
 }
 
+/* K7, tabled and streamed (round 2).  The kernel above rebuilds four stencils
+ * per output (fp64 divides) and re-reads every U row from L2 once per stencil
+ * row: 18.9 ms at config 5, 0.035 of the 16-byte-per-dof roofline.  Here the
+ * 7-slot rows of A and M of both directions are tabled once per plan
+ * (k_apply_tab: slot-major [7][N], weights = -(row entries) as stencil_build
+ * gives them), and a block walks one x-chain (x-element, parity) for 256
+ * columns: per U row it forms t1 = (U M_y)(row, j) and t2 = (U A_y)(row, j)
+ * once (7 coalesced loads), keeps them for the rows c - 1, c, c + 1 in
+ * registers and for the element's two hat rows, and emits
+ * F(row_c, j) = sum_a wA_x[a] t1[a] + wM_x[a] t2[a].  The x-hat rows (7-point
+ * rows) stay with the kernel above. */
+__global__ void k_apply_tab(DirDev o, double half_w2, int* __restrict__ idx, double* __restrict__ wA,
+                            double* __restrict__ wM) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= o.N) return;
+  Stencil a, m;
+  stencil_build(o, l, ST_APPLY, 1.0, half_w2, nullptr, nullptr, a);
+  stencil_build(o, l, ST_APPLY, 0.0, 1.0, nullptr, nullptr, m);
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    idx[(size_t)q * o.N + l] = a.idx[q];  // (A and M have the same pattern)
+    wA[(size_t)q * o.N + l] = a.idx[q] >= 0 ? a.w[q] : 0.0;
+    wM[(size_t)q * o.N + l] = m.idx[q] >= 0 ? m.w[q] : 0.0;
+  }
+}
+
+cudaError_t launch_apply_tab(const DirDev& o, double omega, const ApplyTab& t, cudaStream_t st) {
+  k_apply_tab<<<(o.N + 127) / 128, 128, 0, st>>>(o, 0.5 * omega * omega, const_cast<int*>(t.idx),
+                                                  const_cast<double*>(t.wA), const_cast<double*>(t.wM));
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256, 4) k_apply2d_chain(DirDev x, DirDev y, ApplyTab tx, ApplyTab ty,
+                                                        const double* __restrict__ U, double* __restrict__ F) {
+  extern __shared__ double xw[];  // [10][m]: wA slots 0-4, wM slots 0-4 of the chain's rows
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = blockIdx.y % x.n, pi = blockIdx.y / x.n;
+  const int m = chain_len(x.p, pi);
+  // the chain's x-rows of A and M into shared memory in one round of loads
+  // (read per row from the tables they cost one L2 latency per chain
+  // position: ncu long_scoreboard 36 stalls per issue, 65% of the samples)
+  for (int idx = threadIdx.x; idx < 10 * m; idx += blockDim.x) {
+    const int q = idx / m, c = idx - q * m;
+    const int row = x.nh + (pi + 2 * c) * x.n + e;
+    xw[idx] = q < 5 ? __ldg(tx.wA + (size_t)q * x.N + row) : __ldg(tx.wM + (size_t)(q - 5) * x.N + row);
+  }
+  __syncthreads();
+  if (j >= y.N) return;
+  // y-rows of A and M for column j (absent slots: weight 0, own column)
+  int jy[7];
+  double ya[7], ym[7];
+#pragma unroll
+  for (int b = 0; b < 7; ++b) {
+    const int id = __ldg(ty.idx + (size_t)b * y.N + j);
+    jy[b] = id >= 0 ? id : j;
+    ya[b] = __ldg(ty.wA + (size_t)b * y.N + j);
+    ym[b] = __ldg(ty.wM + (size_t)b * y.N + j);
+  }
+  auto row_t = [&](int row, double& t1, double& t2) {  // (U M_y)(row, j), (U A_y)(row, j), both negated
+    const double* __restrict__ r = U + (size_t)row * y.N;
+    double u[7];
+#pragma unroll
+    for (int b = 0; b < 7; ++b) u[b] = __ldg(r + jy[b]);
+    t1 = 0.0;
+    t2 = 0.0;
+#pragma unroll
+    for (int b = 0; b < 7; ++b) {
+      t1 += ym[b] * u[b];
+      t2 += ya[b] * u[b];
+    }
+  };
+  const int hL = hat_of_node(e, x.n, x.bc), hR = hat_of_node(e + 1, x.n, x.bc);
+  double h1[2] = {0.0, 0.0}, h2[2] = {0.0, 0.0};
+  if (hL >= 0) row_t(hL, h1[0], h2[0]);
+  if (hR >= 0) row_t(hR, h1[1], h2[1]);
+  auto rowc = [&](int c) { return x.nh + (pi + 2 * c) * x.n + e; };
+  double p1 = 0.0, p2 = 0.0, c1 = 0.0, c2 = 0.0, n1 = 0.0, n2 = 0.0;  // rows c - 1, c, c + 1
+  if (m > 0) row_t(rowc(0), c1, c2);
+  // groups of RG rows: the 7 RG loads of the next RG rows are issued together
+  // (one row at a time left a single row of loads in flight per thread)
+  constexpr int RG = 1;
+  constexpr int PF = 8;  // L2 prefetch distance (rows) of the three bubble-column segments
+#pragma unroll
+  for (int c = 2; c < 2 + PF; ++c)
+    if (c < m) {
+      const double* r = U + (size_t)rowc(c) * y.N;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + jy[b]));
+    }
+  for (int c0 = 0; c0 < m; c0 += RG) {
+    if (c0 + 2 + PF < m) {
+      const double* r = U + (size_t)rowc(c0 + 2 + PF) * y.N;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) asm volatile("prefetch.global.L2 [%0];" ::"l"(r + jy[b]));
+    }
+    double u[RG][7];
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+      const int cn = c0 + i + 1 < m ? c0 + i + 1 : m - 1;  // (clamped: unused past the chain)
+      const double* __restrict__ r = U + (size_t)rowc(cn) * y.N;
+#pragma unroll
+      for (int b = 0; b < 7; ++b) u[i][b] = __ldg(r + jy[b]);
+    }
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+      const int c = c0 + i;
+      if (c < m) {
+        n1 = 0.0;
+        n2 = 0.0;
+        if (c + 1 < m) {
+#pragma unroll
+          for (int b = 0; b < 7; ++b) {
+            n1 += ym[b] * u[i][b];
+            n2 += ya[b] * u[i][b];
+          }
+        }
+        double acc = 0.0;  // slots: [0] own row, [1] k - 2, [2] k + 2, [3] hL, [4] hR
+        acc += xw[c] * c1 + xw[5 * m + c] * c2;
+        acc += xw[m + c] * p1 + xw[6 * m + c] * p2;
+        acc += xw[2 * m + c] * n1 + xw[7 * m + c] * n2;
+        acc += xw[3 * m + c] * h1[0] + xw[8 * m + c] * h2[0];
+        acc += xw[4 * m + c] * h1[1] + xw[9 * m + c] * h2[1];
+        F[(size_t)rowc(c) * y.N + j] = acc;
+        p1 = c1;
+        p2 = c2;
+        c1 = n1;
+        c2 = n2;
+      }
+    }
+  }
+}
+
 cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const double* U, double* F,
-                           cudaStream_t st) {
+                           cudaStream_t st, const ApplyTab* tx, const ApplyTab* ty) {
+  if (tx && ty && tx->idx && ty->idx && x.nb > 0) {
+    if (x.nh > 0) {  // the x-hat rows: 7-point rows
+      dim3 gh((y.N + 127) / 128, x.nh);
+      k_apply2d<<<gh, 128, 0, st>>>(x, y, 0.5 * omega * omega, U, F);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    dim3 grid((y.N + 255) / 256, 2 * x.n);
+    k_apply2d_chain<<<grid, 256, sizeof(double) * 10 * chain_len(x.p, 0), st>>>(x, y, *tx, *ty, U, F);
+    return cudaGetLastError();
+  }
   dim3 grid((y.N + 127) / 128, x.N);
   k_apply2d<<<grid, 128, 0, st>>>(x, y, 0.5 * omega * omega, U, F);
   return cudaGetLastError();

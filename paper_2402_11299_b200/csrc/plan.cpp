@@ -359,6 +359,8 @@ struct hpfem_plan_s {
   double* fy = nullptr;           // J+1 sets (y-solves, last = mass)
   double* d_delta = nullptr;      // [n_x | n_y]
   double* d_ldtab = nullptr;      // load-source tables of both directions (DirDev::lw / lr)
+  double* d_aptab = nullptr;      // hpfem_apply's tabled rows of A and M (ApplyTab), both directions
+  ApplyTab apx{nullptr, nullptr, nullptr}, apy{nullptr, nullptr, nullptr};
   double* d_shift = nullptr;      // kap/sig arrays
   double* d_tau = nullptr;        // apply shifts [hw2 - p_j | hw2 + q_j] (K11)
   int* d_err = nullptr;
@@ -453,6 +455,7 @@ void free_plan(hpfem_plan_t pl) {
   cudaFree(pl->fy);
   cudaFree(pl->d_delta);
   cudaFree(pl->d_ldtab);
+  cudaFree(pl->d_aptab);
   cudaFree(pl->d_shift);
   cudaFree(pl->d_tau);
   cudaFree(pl->d_err);
@@ -597,6 +600,18 @@ int build_plan(const double* xs, int nx, int px, const double* ys, int ny, int p
     if ((ce = launch_load_tab(pl->dx, const_cast<int*>(pl->dx.lr), const_cast<double*>(pl->dx.lw), st)) != cudaSuccess ||
         (ce = launch_load_tab(pl->dy, const_cast<int*>(pl->dy.lr), const_cast<double*>(pl->dy.lw), st)) != cudaSuccess)
       return fail_cuda(ce, "load tables");
+  }
+  if (!env_int("HPFEM_NO_APPLY_TAB", 0)) {  // hpfem_apply's row tables ([7][N] idx, wA, wM per direction)
+    const size_t nxy = (size_t)pl->dx.N + pl->dy.N;
+    if ((ce = cudaMalloc(&pl->d_aptab, nxy * 7 * (2 * sizeof(double) + sizeof(int)))) != cudaSuccess)
+      return fail_cuda(ce, "alloc");
+    double* w = pl->d_aptab;
+    int* r = reinterpret_cast<int*>(w + 14 * nxy);
+    pl->apx = ApplyTab{r, w, w + 7 * (size_t)pl->dx.N};
+    pl->apy = ApplyTab{r + 7 * (size_t)pl->dx.N, w + 14 * (size_t)pl->dx.N, w + 14 * (size_t)pl->dx.N + 7 * (size_t)pl->dy.N};
+    if ((ce = launch_apply_tab(pl->dx, omega, pl->apx, st)) != cudaSuccess ||
+        (ce = launch_apply_tab(pl->dy, omega, pl->apy, st)) != cudaSuccess)
+      return fail_cuda(ce, "apply tables");
   }
   // solve orientation (see hpfem_plan_s::swap): transposed when only that
   // makes the half-steps expressible by the TMA kernels (or when forced by
@@ -1135,7 +1150,7 @@ int hpfem_apply(hpfem_plan_t pl, const double* U, double* F, void* cuda_stream) 
   pl->launches = 0;
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const int e0 = prof_mark(pl, st);
-  const int rc = count_launch(pl, launch_apply2d(pl->dx, pl->dy, pl->omega, U, F, st), "apply");
+  const int rc = count_launch(pl, launch_apply2d(pl->dx, pl->dy, pl->omega, U, F, st, &pl->apx, &pl->apy), "apply");
   prof_add(pl, 4, e0, prof_mark(pl, st), 16.0 * pl->hx.N * pl->hy.N);
   return rc;
 }
@@ -1290,7 +1305,7 @@ int transform2d(hpfem_plan_t pl, int inverse, const double* in, double* tmp, dou
 /* F = A_x U M_y + M_x U A_y + <v, c u>, the last by eq. (evaluation) */
 int varcoef_core(hpfem_plan_t pl, const double* cgrid, const double* U, double* F, cudaStream_t st) {
   int rc;
-  if ((rc = count_launch(pl, launch_apply2d(pl->dx, pl->dy, pl->omega, U, F, st), "apply"))) return rc;
+  if ((rc = count_launch(pl, launch_apply2d(pl->dx, pl->dy, pl->omega, U, F, st, &pl->apx, &pl->apy), "apply"))) return rc;
   if ((rc = count_launch(pl, launch_unload2d(pl->dx, pl->dy, U, pl->gs0, st), "unload"))) return rc;
   if ((rc = transform2d(pl, 1, pl->gs0, pl->gs1, pl->gs0, cgrid, st))) return rc;  // c o values
   if ((rc = transform2d(pl, 0, pl->gs0, pl->gs1, pl->gs0, nullptr, st))) return rc;
