@@ -401,7 +401,7 @@ struct hpfem_plan_s {
   double* h_sc = nullptr;         // pinned host copy of one scalar
   // CUDA graphs of whole ADI solves (launch-bound small problems), keyed by
   // (workspace, F, U, iters); captured on a plan-owned stream, launched on the caller's
-  struct GraphEntry { const Workspace* w; const double* F; double* U; int iters; cudaGraphExec_t exec; long long launches; };
+  struct GraphEntry { const void* w; const double* F; double* U; int iters; cudaGraphExec_t exec; long long launches; };
   std::vector<GraphEntry> graphs;
   cudaStream_t cap = nullptr;
 };
@@ -972,18 +972,23 @@ static void build_steps(hpfem_plan_t pl, const Workspace& w, int iters, std::vec
   out.push_back({Fin, true, -1, 2});
 }
 
-/* Algorithm 2 on one workspace (validated arguments, iters >= 1) */
-static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, double* U, int iters, cudaStream_t st) {
+/* Algorithm 2 on one workspace (validated arguments, iters >= 1), in three
+ * parts: copy-in (the only kernels that read F), the 2 iters + 1 line-solve
+ * passes (workspace buffers only), finalize (the only kernels that write U). */
+static int solve_pre(hpfem_plan_t pl, const Workspace& w, const double* F, cudaStream_t st) {
   int rc;
-  {
-    const int e0 = prof_mark(pl, st);
-    if (pl->swap) {  // G^T into the scratch iterate X2 (dead until half-step B writes it)
-      if ((rc = count_launch(pl, launch_transpose(F, pl->hx.N, pl->hy.N, w.X2, st), "transpose"))) return rc;
-      F = w.X2;
-    }
-    if ((rc = count_launch(pl, launch_copyin(pl->ox, pl->oy, pl->lay, F, w.Gp, st), "copy-in"))) return rc;
-    prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);  // layout change, not algorithmic
+  const int e0 = prof_mark(pl, st);
+  if (pl->swap) {  // G^T into the scratch iterate X2 (dead until half-step B writes it)
+    if ((rc = count_launch(pl, launch_transpose(F, pl->hx.N, pl->hy.N, w.X2, st), "transpose"))) return rc;
+    F = w.X2;
   }
+  if ((rc = count_launch(pl, launch_copyin(pl->ox, pl->oy, pl->lay, F, w.Gp, st), "copy-in"))) return rc;
+  prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);  // layout change, not algorithmic
+  return HPFEM_OK;
+}
+
+static int solve_mid(hpfem_plan_t pl, const Workspace& w, int iters, cudaStream_t st) {
+  int rc;
   std::vector<StepRec> steps;
   build_steps(pl, w, iters, steps);
   NvtxRange solve_range("hpfem_solve");
@@ -991,14 +996,25 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
     NvtxRange nr(r.fin ? "final W_J C^-1" : (r.P.dir == 1 ? "ADI half-step A (y-solves)" : "ADI half-step B (x-solves)"));
     if ((rc = run_step(pl, w, r.P, st, r.fin, r.ia_g, r.ia_w))) return rc;
   }
-  const StepParams& Fin = steps.back().P;
+  return HPFEM_OK;
+}
+
+static int solve_post(hpfem_plan_t pl, const Workspace& w, double* U, cudaStream_t st) {
+  const FacView fin = fview(pl, 1, pl->J);  // the final mass solve's correction vectors
   const int e0 = prof_mark(pl, st);
   // (swap: U^T into the dead iterate X2, then transposed into U)
-  rc = count_launch(pl, launch_finalize(pl->ox, pl->oy, pl->lay, Fin.f.vL, Fin.f.vR, w.X1, pl->swap ? w.X2 : U, st),
-                    "finalize");
+  int rc = count_launch(pl, launch_finalize(pl->ox, pl->oy, pl->lay, fin.vL, fin.vR, w.X1, pl->swap ? w.X2 : U, st),
+                        "finalize");
   if (!rc && pl->swap) rc = count_launch(pl, launch_transpose(w.X2, pl->ox.N, pl->oy.N, U, st), "transpose");
   prof_add(pl, 2, e0, prof_mark(pl, st), 0.0);
   return rc;
+}
+
+static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, double* U, int iters, cudaStream_t st) {
+  int rc;
+  if ((rc = solve_pre(pl, w, F, st))) return rc;
+  if ((rc = solve_mid(pl, w, iters, st))) return rc;
+  return solve_post(pl, w, U, st);
 }
 
 /* solve_core replayed from a CUDA graph: the whole solve (6J + 3 kernels and
@@ -1008,11 +1024,22 @@ static int solve_core(hpfem_plan_t pl, const Workspace& w, const double* F, doub
  * kernels with the same arguments.  Not used while profiling (per-launch
  * events) or with HPFEM_NO_GRAPH=1; at most kMaxGraphs cached. */
 static int solve_graph(hpfem_plan_t pl, const Workspace& w, const double* F, double* U, int iters,
-                       cudaStream_t st) {
-  if (pl->tun.no_graph || !pl->ev.empty()) return solve_core(pl, w, F, U, iters, st);
+                       cudaStream_t st, bool mid_only = false) {
+  // mid_only (hpfem_solve_batched): the graph holds the line-solve passes only
+  // -- they touch the workspace's buffers and nothing else, so one graph per
+  // stream slot serves every right-hand side; copy-in and finalize are
+  // launched around it.  Keyed by the workspace's Gp (the slots live in a
+  // vector that may move them).
+  if (pl->tun.no_graph || !pl->ev.empty())
+    return mid_only ? solve_mid(pl, w, iters, st) : solve_core(pl, w, F, U, iters, st);
   cudaError_t ce;
+  const void* key = mid_only ? (const void*)w.Gp : (const void*)&w;
+  if (mid_only) {
+    F = nullptr;
+    U = nullptr;
+  }
   for (auto& g : pl->graphs)
-    if (g.w == &w && g.F == F && g.U == U && g.iters == iters) {
+    if (g.w == key && g.F == F && g.U == U && g.iters == iters) {
       if ((ce = cudaGraphLaunch(g.exec, st)) != cudaSuccess) return cuda_err(ce, "graph launch");
       pl->launches += g.launches;
       return HPFEM_OK;
@@ -1022,7 +1049,7 @@ static int solve_graph(hpfem_plan_t pl, const Workspace& w, const double* F, dou
   if ((ce = cudaStreamBeginCapture(pl->cap, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
     return cuda_err(ce, "begin capture");
   const long long l0 = pl->launches;
-  int rc = solve_core(pl, w, F, U, iters, pl->cap);
+  int rc = mid_only ? solve_mid(pl, w, iters, pl->cap) : solve_core(pl, w, F, U, iters, pl->cap);
   cudaGraph_t graph = nullptr;
   ce = cudaStreamEndCapture(pl->cap, &graph);
   if (rc) {
@@ -1034,12 +1061,12 @@ static int solve_graph(hpfem_plan_t pl, const Workspace& w, const double* F, dou
   ce = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
   if (ce != cudaSuccess) return cuda_err(ce, "graph instantiate");
-  constexpr size_t kMaxGraphs = 4;
+  constexpr size_t kMaxGraphs = 16;  // (up to 8 stream slots of hpfem_solve_batched + single solves)
   if (pl->graphs.size() >= kMaxGraphs) {
     cudaGraphExecDestroy(pl->graphs.front().exec);
     pl->graphs.erase(pl->graphs.begin());
   }
-  pl->graphs.push_back({&w, F, U, iters, exec, pl->launches - l0});
+  pl->graphs.push_back({key, F, U, iters, exec, pl->launches - l0});
   if ((ce = cudaGraphLaunch(exec, st)) != cudaSuccess) return cuda_err(ce, "graph launch");
   return HPFEM_OK;
 }
@@ -1125,7 +1152,12 @@ int hpfem_solve_batched(hpfem_plan_t pl, int batch, const double* F, double* U, 
   for (int b = 0; b < batch; ++b) {
     const Workspace& w = pl->bws[b % slots];
     pl->launches = 0;
-    const int rc = solve_core(pl, w, F + (size_t)b * nn, U + (size_t)b * nn, pl->J, w.st);
+    // copy-in, the slot's graph of the line-solve passes (one graph launch
+    // instead of 6J + 1 kernel launches: the batch is launch-bound otherwise),
+    // finalize
+    int rc = solve_pre(pl, w, F + (size_t)b * nn, w.st);
+    if (rc == HPFEM_OK) rc = solve_graph(pl, w, nullptr, nullptr, pl->J, w.st, true);
+    if (rc == HPFEM_OK) rc = solve_post(pl, w, U + (size_t)b * nn, w.st);
     total += pl->launches;
     if (rc != HPFEM_OK) return rc;
   }
