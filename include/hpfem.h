@@ -152,13 +152,16 @@ int hpfem_solve_iters(hpfem_plan_t plan, const double* F, double* U, int iters, 
  * internal streams, each with its own workspace (allocated on first use and
  * kept by the plan: 3 N_x x ld arrays per stream), forked from and joined
  * back into cuda_stream, so the call is ordered like any other work on
- * cuda_stream.  Each U_b is bitwise what hpfem_solve(F_b) returns.
+ * cuda_stream.  Each stream replays one CUDA graph of the line-solve passes
+ * per right-hand side.  Each U_b is bitwise what hpfem_solve(F_b) returns.
  * EINVAL also when profiling is on (hpfem_plan_profile records on one
  * stream).  batch = 0 is a no-op. */
 int hpfem_solve_batched(hpfem_plan_t plan, int batch, const double* F, double* U, void* cuda_stream);
 
 /* hpfem_apply -- F = A_x U M_y + M_x U A_y (the operator of eq. adi:poisson,
- * P:L658-L664).  U, F device pointers, N_x x N_y, must not overlap. */
+ * P:L658-L664).  U, F device pointers, N_x x N_y, must not overlap.  The
+ * rows of A and M are tabled at plan time (HPFEM_NO_APPLY_TAB=1: built per
+ * output, the round-1 kernel). */
 int hpfem_apply(hpfem_plan_t plan, const double* U, double* F, void* cuda_stream);
 
 /* hpfem_load -- G = R_x^T M_{P,x} F_leg M_{P,y} R_y.
@@ -247,7 +250,9 @@ int hpfem_imex_step(hpfem_plan_t plan, double dt, const double* U_leg, double* U
  * batched solves of the 1D screened Poisson discretisation
  *        (K + w^2 M) u = f      (Dirichlet basis Q, Neumann C or mixed)
  * with the reverse Cholesky factor of Algorithm 1 in static-
- * condensation form (one CTA per right-hand side).
+ * condensation form (one CTA per one or two right-hand sides; for small
+ * batches one thread-block cluster per right-hand side, the row held in its
+ * distributed shared memory -- same result to rounding).
  *   hpfem_plan1d: breakpoints xs[0..n] (host, strictly increasing), degree
  *     p >= 2, bc = a 1D code HPFEM_BC_DIRICHLET .. HPFEM_BC_NEUMANN_DIRICHLET,
  *     omega (Neumann at both ends needs omega != 0); factors on the device and

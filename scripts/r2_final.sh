@@ -17,5 +17,7 @@ python scripts/prof_solve.py 5 2 > /dev/null 2>&1 && ncu --set full --clock-cont
 python scripts/prof_solve.py 4 2 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_[xy]step_tma|k_hats_rows|k_hats_cols" -s 6 -c 8 -o gpurun_out/r02_config4_full python scripts/prof_solve.py 4 2 > gpurun_out/r02_ncu_full4.log 2>&1; echo full4 rc=$?
 python scripts/ncu_summary.py gpurun_out/r02_config5_full.ncu-rep > gpurun_out/r02_config5_ncu.txt
 python scripts/ncu_summary.py gpurun_out/r02_config4_full.ncu-rep > gpurun_out/r02_config4_ncu.txt
+for k in k_ystep_tma k_xstep_tma k_hats_rows k_hats_cols; do echo "== $k"; python scripts/ncu_lines.py gpurun_out/r02_config5_full.ncu-rep $k 12; done > gpurun_out/r02_config5_ncu_lines.txt 2>&1
+rm -f gpurun_out/r02_config5_full.ncu-rep gpurun_out/r02_config4_full.ncu-rep  # (gpurun brings back at most 64 MiB)
 python scripts/launch_summary.py gpurun_out/r02_config5_launches.csv > gpurun_out/r02_config5_launches.txt
 python scripts/launch_summary.py gpurun_out/r02_config4_launches.csv > gpurun_out/r02_config4_launches.txt
