@@ -395,12 +395,19 @@ def run_ours(args, cfg):
     # ---- roofline of the dominant kernel (half-step bubble kernel K2-K4)
     peak, peak_kind = measured_peak()
     kb = {k: prof["halfstep_bubbles_x"][k] + prof["halfstep_bubbles_y"][k] for k in ("ms", "launches", "bytes")}
+    pth = plan.path()
+    kernel_label = {
+        "tma": "k_xstep_tma / k_ystep_tma (K2: TMA-fed half-step kernels, fused apply + bubble-chain solve)"
+               + (", transposed solve" if pth["transposed"] else ""),
+        "ldg": "k_bubbles<0> / k_bubbles<1> (K2, LDG streaming variant)",
+        "small": "k_adi_small (K11: whole solve in one CTA; no per-kernel times)",
+    }.get(pth["path"], str(pth["path"]))
     achieved = kb["bytes"] / (kb["ms"] / 1e3) / 1e9 if kb["ms"] > 0 else None
     traffic, traffic_src = ncu_traffic(cfg.idx)
     total_kernel_ms = sum(v["ms"] for v in prof.values())
     alg_bytes_step = 8.0 * Nx * Ny * (6 * J + 1)
     roofline = {
-        "bound": "hbm", "kernel": "k_bubbles (fused apply + bubble-chain solve, K2-K4)",
+        "bound": "hbm", "kernel": kernel_label,
         "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": (achieved / peak) if achieved else None, "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
         "traffic": traffic, "traffic_source": traffic_src,
