@@ -296,6 +296,30 @@ __device__ __forceinline__ void stencil_build(const DirDev& o, int l, int mode, 
   }
 }
 
+/* the stencil rows of HAT row t alone (the idx[] stencil_build gives for
+ * l = t < nh), without the weights' floating-point work */
+__device__ __forceinline__ void hat_row_idx(const DirDev& o, int t, int mode, int* idx) {
+#pragma unroll
+  for (int q = 0; q < 7; ++q) idx[q] = -1;
+  if (mode == ST_NONE) return;
+  idx[0] = t;
+  if (mode == ST_CORR) return;
+  const int n = o.n, nh = o.nh;
+  const int node = node_of_hat(t, o.bc);
+  const int eL = node - 1, eR = node;
+  const bool k1 = o.p - 2 >= 1;
+  if (eL >= 0) {
+    if (hat_of_node(node - 1, n, o.bc) >= 0) idx[1] = t - 1;
+    idx[3] = nh + eL;
+    if (k1) idx[4] = nh + n + eL;
+  }
+  if (eR <= n - 1) {
+    if (hat_of_node(node + 1, n, o.bc) >= 0) idx[2] = t + 1;
+    idx[5] = nh + eR;
+    if (k1) idx[6] = nh + n + eR;
+  }
+}
+
 /* internal column of y-dof d */
 __host__ __device__ __forceinline__ int ycol_ke(const Layout& L, int k, int e) {
   return L.emaj ? L.hb + e * L.Q + k : L.hb + k * L.np + e;
@@ -845,24 +869,22 @@ __global__ void __launch_bounds__(128) k_hatrows_y(StepParams P) {
   double* fac = sh + 8 * W;               // [EGH][2][cfs]
   __shared__ int s_idx[7];
   __shared__ double s_w[7];
-  if (threadIdx.x == 0) {
-    Stencil st;
-    stencil_build(x, t, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
-    for (int q = 0; q < 7; ++q) {
-      s_idx[q] = st.idx[q];
-      s_w[q] = st.w[q];
-    }
-  }
   __shared__ __align__(8) uint64_t bar;
   const int nw = ne * L.Q;
   const int cfs = P.f.cfs;
+  // Thread 0 needs only the stencil's ROWS (integer logic) to issue the bulk
+  // copies; the weights (fp64 divides, ~1.5 us on one thread) are built by
+  // warp 1 while the copies are in flight.
+  if (threadIdx.x == 32) {
+    Stencil st;
+    stencil_build(x, t, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
+    for (int q = 0; q < 7; ++q) s_w[q] = st.w[q];
+  }
   if (threadIdx.x == 0) {
+    hat_row_idx(x, t, P.mode, s_idx);
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  // bulk copies of the G segment, the stencil rows and the chains' factors (one thread)
-  if (threadIdx.x == 0) {
+    // bulk copies of the G segment, the stencil rows and the chains' factors
     uint32_t bytes = 2 * ne * cfs * 8;
     for (int q = 0; q < 8; ++q)
       if (q == 0 ? P.alphaG != 0.0 : s_idx[q - 1] >= 0) bytes += nw * 8;
@@ -874,6 +896,7 @@ __global__ void __launch_bounds__(128) k_hatrows_y(StepParams P) {
     }
     bulk_load(fac, P.f.cf + (size_t)2 * e0 * cfs, 2 * ne * cfs * 8, &bar);
   }
+  __syncthreads();  // s_idx, s_w and the barrier are visible
   // segments without a source read as zero
   for (int q = 0; q < 8; ++q) {
     const bool has = q == 0 ? P.alphaG != 0.0 : s_idx[q - 1] >= 0;
@@ -990,23 +1013,21 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
       R[2 * ei + 1] = v.y;  // bubble 1
     }
   }
-  mbar_wait(&bar, 0);
-  __syncthreads();
   // right-hand sides and the chain solves split over the 8 warps: thread
   // (column j, warp w) owns chain positions [w BP, w BP + BP) of column j;
   // the block maps of the two recurrences are folded through shared memory
-  // (the x chains run to 128 positions on the transposed path)
+  // (the x chains run to 128 positions on the transposed path).  The column's
+  // stencil (fp64 divides) is built while the copies are in flight.
   {
     const int j = threadIdx.x & 31, w = threadIdx.x >> 5;
     const bool act = j < nl;
     double* fa = fac + cfs;  // [8][32] block maps (after the factors)
     double* fbm = fa + 8 * 32;
     const int BP = (m + 7) >> 3, ca = w * BP, cb = min(m, ca + BP);
+    Stencil st;
+    int off[7];
     if (act) {
-      const int l = l0 + j;
-      Stencil st;
-      stencil_build(y, l, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
-      int off[7];
+      stencil_build(y, l0 + j, P.mode, P.kap_a, P.tau, P.cvL, P.cvR, st);
 #pragma unroll
       for (int q = 0; q < 7; ++q) {
         const int d = st.idx[q];
@@ -1020,6 +1041,10 @@ __global__ void __launch_bounds__(256) k_hatcols_x(StepParams P) {
           off[q] = TC + HREG + 2 * (e - elo) + k;
         }
       }
+    }
+    mbar_wait(&bar, 0);
+    __syncthreads();
+    if (act) {
       const double aG = P.alphaG;
       // right-hand sides in place (each thread reads its stencil columns and
       // overwrites only its own G slot)
