@@ -1214,7 +1214,26 @@ __global__ void __launch_bounds__(256, 2) k_hats_rows(StepParams P) {
   for (int lp = (P.hl_end <= 0 ? 0 : P.hl_begin) + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); lp < lp_hi; lp += nwarps) {
     const int l = row_of(P.o, lp);
     Stencil st;
-    line_stencil<1>(P, l, st);
+    if (P.wtab && P.mode == ST_APPLY && l >= P.o.nh) {
+      // bubble row (k, e): the five weights the bubble kernel uses (k_wtab_y:
+      // [e][pi][kh][6], the same expressions as stencil_build) instead of
+      // rebuilding them with fp64 divides on every lane; the rows from (k, e)
+      const DirDev& o = P.o;
+      const int b = l - o.nh, k = b / o.n, e = b - k * o.n;
+      const double* wt = P.wtab + (((size_t)e * 2 + (k & 1)) * chain_len(o.p, 0) + (k >> 1)) * 6;
+      const int hL = hat_of_node(e, o.n, o.bc), hR = hat_of_node(e + 1, o.n, o.bc);
+      st.idx[0] = l;
+      st.idx[1] = k >= 2 ? l - 2 * o.n : -1;
+      st.idx[2] = k + 2 <= o.p - 2 ? l + 2 * o.n : -1;
+      st.idx[3] = hL;
+      st.idx[4] = hR;
+      st.idx[5] = st.idx[6] = -1;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) st.w[q] = __ldg(wt + q);
+      st.w[5] = st.w[6] = 0.0;
+    } else {
+      line_stencil<1>(P, l, st);
+    }
     // right-hand sides r_h - B z for t = lane + 32 i; all loads of a chunk of
     // HC hats issued before the FMAs (absent stencil rows clamped, skipped)
     constexpr int HC = HB < 4 ? HB : 2;  // no register spills at 128 registers
@@ -1346,7 +1365,24 @@ __global__ void __launch_bounds__(256, 2) k_hats_cols(StepParams P, int col_begi
   __syncthreads();
   if (l >= 0) {
     Stencil st;
-    line_stencil<0>(P, l, st);
+    if (P.wtab && P.mode == ST_APPLY && P.lay.emaj && l >= P.o.nh) {
+      // bubble column (k, e): the bubble kernel's tabled weights (k_wtab_x:
+      // [e][5][Q], the same expressions as stencil_build), internal columns
+      const DirDev& o = P.o;
+      const int b = l - o.nh, k = b / o.n, e = b - k * o.n;
+      const double* wt = P.wtab + (size_t)e * 5 * P.lay.Q + k;
+      st.idx[0] = li;
+      st.idx[1] = k >= 2 ? li - 2 : -1;
+      st.idx[2] = k + 2 <= o.p - 2 ? li + 2 : -1;
+      st.idx[3] = hat_of_node(e, o.n, o.bc);      // (hat t sits at internal column t)
+      st.idx[4] = hat_of_node(e + 1, o.n, o.bc);
+      st.idx[5] = st.idx[6] = -1;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) st.w[q] = __ldg(wt + (size_t)q * P.lay.Q);
+      st.w[5] = st.w[6] = 0.0;
+    } else {
+      line_stencil<0>(P, l, st);
+    }
     const double* __restrict__ G = P.G;
     const double* __restrict__ Xp = P.Xp;
     const double* __restrict__ Z = P.out;  // chain-first bubbles of this half-step
