@@ -1798,7 +1798,7 @@ __global__ void __launch_bounds__(256, 4) k_apply2d_chain(DirDev x, DirDev y, Ap
 
 cudaError_t launch_apply2d(const DirDev& x, const DirDev& y, double omega, const double* U, double* F,
                            cudaStream_t st, const ApplyTab* tx, const ApplyTab* ty) {
-  if (tx && ty && tx->idx && ty->idx && x.nb > 0) {
+  if (tx && ty && tx->idx && ty->idx && x.nb > 0 && sizeof(double) * 10 * chain_len(x.p, 0) <= 48 * 1024) {
     if (x.nh > 0) {  // the x-hat rows: 7-point rows
       dim3 gh((y.N + 127) / 128, x.nh);
       k_apply2d<<<gh, 128, 0, st>>>(x, y, 0.5 * omega * omega, U, F);
