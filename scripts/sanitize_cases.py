@@ -6,7 +6,9 @@ synccheck / racecheck / initcheck, one tool per run):
 Covers K11 (config 1), the LDG half-step kernels (config 1 without K11), the
 TMA ring kernels k_xstep_tma / k_ystep_tma with short (config 2, CL = 16)
 and full-length chains (CL = 64, the config-5 kernel shape), the hat-line and
-hat Schur kernels, load / unload / apply, the 1D solver and a batched solve.
+hat Schur kernels, load / unload / apply, the two-threads-per-chain x kernel
+(natively and on the transposed path), the 1D solver (cluster form and
+row-per-CTA form) and a batched solve.
 Each result is checked against the oracle (L2 <= 1e-10), so a tool that
 perturbs the run cannot pass silently.  HPFEM_NO_GRAPH=1: kernels are
 launched directly (one sanitizer record per launch)."""
@@ -59,6 +61,33 @@ run("config 2 TMA CL=16", x2, c2.px, y2, c2.py, c2.omega, c2.bc, c2.tol)
 g6, g5 = W.graded_mesh(0, 1, 6, 0.85), W.graded_mesh(0, 1, 5, 0.85)
 run("graded p=128 Neumann TMA CL=64", g6, 128, g5, 128, 1.0, 1, 1e-10)
 run("p=150 LDG long chains", np.linspace(0, 1, 3), 150, np.linspace(0, 1, 2), 140, 0.5, 0, 1e-8)
+# round 2: chains of 65-128 positions with two threads per chain (k_xstep_tma2), natively and transposed
+rng = np.random.default_rng(45)
+
+
+def rmesh(n, a, b):
+    w = rng.uniform(0.3, 1.7, size=n)
+    xs = np.concatenate([[0.0], np.cumsum(w)])
+    return a + (b - a) * xs / xs[-1]
+
+
+run("p_x=130 two threads per x chain", rmesh(2, 0, 1), 130, rmesh(7, 0, 1), 18, 1.0, 1, 1e-10)
+run("p_y=200 transposed, two threads per chain", rmesh(4, 0, 1), 20, rmesh(3, 0, 1), 200, 1.0, 0, 1e-10)
+# 1D solver: cluster form (clusters of 1 and 2 CTAs), row-per-CTA form with two rows per CTA
+for xs1, p1, nrhs, env in ((np.linspace(0, 1, 9), 8, 4, "1"), (np.linspace(0, 1, 513), 33, 3, "1"),
+                           (np.linspace(0, 1, 41), 5, 601, "0")):
+    os.environ["HPFEM_1D_CLUSTER"] = env
+    pl = hp.Plan1D(xs1, p1, 0, 1.0)
+    F = torch.randn((nrhs, pl.N), dtype=torch.float64, device="cuda")
+    Uo = torch.empty_like(F)
+    pl.solve(F, Uo)
+    torch.cuda.synchronize()
+    ref = oracle.solve1d(xs1, p1, 0, 1.0, 1.0, F.cpu().numpy())
+    err = np.linalg.norm(Uo.cpu().numpy() - ref) / np.linalg.norm(ref)
+    print(f"1D n={len(xs1) - 1} p={p1} rows={nrhs} cluster={env}: rel err {err:.2e}", flush=True)
+    assert err <= 1e-10
+    pl.close()
+os.environ.pop("HPFEM_1D_CLUSTER", None)
 # 1D solver and batched solve
 pl = hp.Plan1D(np.linspace(0, 1, 9), 8, 0, 1.0)
 F = torch.randn((4, pl.N), dtype=torch.float64, device="cuda")
