@@ -1,4 +1,5 @@
-"""hpfem_apply (K7, F = A_x U M_y + M_x U A_y) timing against its 16-byte-per-dof roofline:
+"""hpfem_apply (K7, F = A_x U M_y + M_x U A_y), hpfem_load (K8) and hpfem_unload (K9) timings against their
+one-read-one-write rooflines:
     python scripts/bench_apply.py [CONFIG ...]"""
 import json
 import os
@@ -33,7 +34,27 @@ for ci in [int(a) for a in sys.argv[1:]] or [2, 3, 4, 5]:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     gbs = 16.0 * plan.Nx * plan.Ny / (ms / 1e3) / 1e9
-    print(json.dumps({"config": ci, "N": [plan.Nx, plan.Ny], "apply_ms": ms, "dof_per_s": plan.Nx * plan.Ny / (ms / 1e3),
-                      "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                                   "bytes_per_dof": 16}}), flush=True)
+    res = {"config": ci, "N": [plan.Nx, plan.Ny], "apply_ms": ms, "dof_per_s": plan.Nx * plan.Ny / (ms / 1e3),
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                        "bytes_per_dof": 16}}
+    # K8 load (G = R^T M_P F_leg M_P R) and K9 unload (C_leg = R U R^T): one read of the
+    # source array + one write of the result
+    nl, ml = (c.px + 1) * (len(xs) - 1), (c.py + 1) * (len(ys) - 1)
+    Fl = torch.randn(nl, ml, dtype=torch.float64, device="cuda")
+    Cl = torch.empty_like(Fl)
+    for name, fn in (("load", lambda: plan.load(Fl, F)), ("unload", lambda: plan.unload(U, Cl))):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / reps
+        by = 8.0 * (nl * ml + plan.Nx * plan.Ny)
+        res[name + "_ms"] = t
+        res[name + "_roofline"] = {"bound": "hbm", "achieved": by / (t / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                                   "frac": by / (t / 1e3) / 1e9 / peak, "bytes": by}
+    print(json.dumps(res), flush=True)
     plan.close()
