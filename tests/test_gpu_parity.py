@@ -236,6 +236,32 @@ def test_config_apply(i):
     assert np.abs(F - Fref).max() <= 1e-12 * np.abs(Fref).max()
 
 
+@pytest.mark.parametrize("tab", ["tabled", "inline"])
+@pytest.mark.parametrize("case", range(len(SMALL)))
+def test_small_apply_load_unload(case, tab, monkeypatch):
+    """hpfem_apply (K7: the tabled chain kernel, and the round-1 kernel with
+    HPFEM_NO_APPLY_TAB=1), hpfem_load (K8) and hpfem_unload (K9) vs the oracle on
+    every small shape: N = 1, single elements (no hats), p = 2 (empty odd
+    chains), ragged column tiles, graded / mixed ends, chains of up to 128
+    positions."""
+    if tab == "inline":
+        monkeypatch.setenv("HPFEM_NO_APPLY_TAB", "1")
+    xs, px, ys, py, om, bc, tol = SMALL[case]
+    plan = gpu_plan(xs, px, ys, py, om, bc, tol)
+    U = W.random_field((plan.Nx, plan.Ny), 70 + case)
+    F = gpu_apply(plan, U)
+    Fref = oracle.apply(xs, px, ys, py, om, bc, U)
+    assert np.abs(F - Fref).max() <= 1e-12 * np.abs(Fref).max()
+    if tab == "tabled":
+        Fleg = W.random_field(((px + 1) * (xs.size - 1), (py + 1) * (ys.size - 1)), 80 + case)
+        G = gpu_load(plan, Fleg)
+        Gref = oracle.load(xs, px, ys, py, bc, Fleg)
+        assert np.abs(G - Gref).max() <= 1e-14 * max(np.abs(Gref).max(), 1e-300)
+        C = gpu_unload(plan, U)
+        Cref = oracle.unload(xs, px, ys, py, bc, U)
+        assert np.abs(C - Cref).max() <= 1e-14 * max(np.abs(Cref).max(), 1e-300)
+
+
 @pytest.mark.parametrize("case", MIXED)
 def test_mixed_apply_load(case):
     """hpfem_apply and hpfem_load with mixed Dirichlet / Neumann ends vs the
